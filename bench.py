@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Headline benchmark: neural photon-field rendering, BASELINE config 2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full frame of render_neural (Alg. 2): 1920x1080, 8 spp, 256^3
+synthetic volume, one point light, paper-size photon field (16x8 hash grid,
+T = 2^19, 5x64 MLP), FAST mode (binary32 delta tracking + ratio-tracked NEE).
+N > 1: image tiles are interleaved over the ranks (strong scaling of one
+frame) and gathered to rank 0 over NCCL.  Timing: W untimed warm-up frames,
+then K frames, each bracketed by CUDA events on the render stream with an L2
+flush (256 MiB write) between frames; barrier + synchronize around the timed
+region; the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+W_, H_, SPP, VOL_N, SEED = 1920, 1080, 8, 256, 2024
+METRIC = "frames/s at 1920x1080, 8 spp, 256^3 volume (neural render, Alg. 2)"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def scene_inputs():
+    from paper_2304_07338_b200.scene import CameraSpec, default_lights, synth_volume, tf_scene_a
+    return synth_volume("sphere_sinusoid", VOL_N), tf_scene_a(), default_lights(), CameraSpec(W_, H_)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clocks sampling (NVML) during the timed region."""
+
+    def __init__(self, dev: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k, None): v for k, v in [
+            ("nvmlClocksEventReasonHwSlowdown", "hw_slowdown"),
+            ("nvmlClocksEventReasonHwThermalSlowdown", "hw_thermal_slowdown"),
+            ("nvmlClocksEventReasonSwThermalSlowdown", "sw_thermal_slowdown"),
+            ("nvmlClocksEventReasonSwPowerCap", "sw_power_cap"),
+            ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown")] if getattr(nv, k, None)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ reference ----
+
+def reference_cpu_frame_sample(rows: int, workers: int, fc, params, vol, tf, lights, cam_spec):
+    """The reference CPU render path on a band of `rows` rows of the frame."""
+    from oracle import oracle as o
+    from paper_2304_07338_b200 import RenderConfig
+    sc = o.RefScene(vol, tf, 100.0)
+    rc = RenderConfig(spp=SPP, g=0.0, seed=SEED, mode="parity", use_field=True)
+    y0 = (H_ - rows) // 2
+    t0 = time.perf_counter()
+    o.ref_render_neural(sc, lights, fc, params, cam_spec, rc, rect=(0, y0, W_, y0 + rows),
+                        workers=workers)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_kind():
+    from oracle import oracle as o
+    return "reference" if o.ref_available() else "port"
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU path timed on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as o
+    from paper_2304_07338_b200 import FieldConfig
+    workers = os.cpu_count() or 1
+    if not o.ref_available():
+        kind = "port"
+    else:
+        kind = "reference"
+    vol, tf, lights, cam = scene_inputs()
+    fc = FieldConfig.paper()
+    params = fc.init_params(seed=SEED, embed_scale=1e-2, bias_scale=0.0)
+    # size the per-step row band to ~3 s of CPU work
+    rows = 4
+    t = reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam)
+    rows = int(min(H_, max(4, rows * 3.0 / max(t, 1e-3))))
+    for _ in range(args.warmup):
+        reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam)
+    times = [reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam)
+             for _ in range(args.steps)]
+    sec_per_frame = float(np.mean(times)) * H_ / rows
+    fps = 1.0 / sec_per_frame
+    sample = (f"{rows} of {H_} rows x {W_} px x {SPP} spp per step (full per-sample program: "
+              f"pf::delta_track + pf::transmittance via pf::parallel_chunks, fp64 field forward); "
+              f"frame time extrapolated by rows")
+    line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_per_frame * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "config 2: 256^3 sphere_sinusoid, 1920x1080, 8 spp, scene A TF, "
+                                   "1 light, paper field", "cpu": "host cores"},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ ours ----
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_07338_b200 import Context, FieldConfig, RenderConfig
+    from paper_2304_07338_b200 import build as pfbuild
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    if not (ROOT / "paper_2304_07338_b200" / "libpfgpu.so").exists():
+        if rank == 0:
+            pfbuild.build()
+        if world > 1:
+            dist.barrier()
+
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = Context(local, stream=stream.cuda_stream)
+    vol, tf, lights, cam_spec = scene_inputs()
+    ctx.upload_volume(vol)
+    ctx.set_medium(tf, 100.0)
+    ctx.set_lights(lights)
+    fc = FieldConfig.paper()
+    params = fc.init_params(seed=SEED, embed_scale=1e-2, bias_scale=0.0)
+    ctx.load_field(fc, params)
+    cam = ctx.camera(cam_spec)
+    rc = RenderConfig(spp=SPP, g=0.0, seed=SEED, mode=args.mode, use_field=True, tile=(16, 16),
+                      shard_index=rank, shard_count=world)
+    frame = torch.zeros((H_, W_, 3), dtype=torch.float32, device="cuda")
+    n_tiles_max = max(ctx.tiles_count(cam, rc, s) for s in range(world))
+    per_shard = n_tiles_max * 16 * 16 * 3
+    packed = torch.zeros(per_shard, dtype=torch.float32, device="cuda")
+    gathered = torch.zeros(per_shard * world, dtype=torch.float32, device="cuda") if world > 1 else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    ctx.set_timing(True)
+
+    def step(stats=True):
+        st = ctx.render_neural(cam, rc, out=frame, stats=stats)
+        if world > 1:
+            ctx.tiles_pack(cam, rc, frame, packed)
+            dist.all_gather_into_tensor(gathered, packed)
+            if rank == 0:
+                ctx.tiles_unpack(cam, rc, gathered, per_shard, frame)
+        return st[1] if stats else None
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    stats = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))                     # L2 flush between timed frames (untimed)
+            ev[i][0].record()
+            stats.append(step())
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - t_wall0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    fps = 1000.0 / ms_per_step
+
+    # per-kernel (this rank): trace kernel dominates; algorithmic bytes = 32 B / tentative step
+    tr_ms = float(np.mean([s["ms_trace"] for s in stats]))
+    fld_ms = float(np.mean([s["ms_field"] for s in stats]))
+    steps_tot = float(np.mean([s["primary_steps"] + s["shadow_steps"] for s in stats]))
+    hits = float(np.mean([s["hits"] for s in stats]))
+    samples = float(np.mean([s["samples"] for s in stats]))
+    peaks, peak_kind = load_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    achieved = steps_tot * 32.0 / (tr_ms * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("k_render_trace_fast" if args.mode == "fast"
+                                                    else "k_render_trace_parity")
+
+    # ---- e2e: public API with host buffers (per-frame TF/light/camera in, frame out)
+    e2e = None
+    if rank == 0 or world > 1:
+        host_frame = torch.empty((H_, W_, 3), dtype=torch.float32, pin_memory=True)
+        tf_h = torch.from_numpy(tf.copy()).pin_memory()
+        li_h = torch.from_numpy(lights.copy()).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_times = []
+        for i in range(args.steps):
+            t0 = time.perf_counter()
+            ctx.set_medium(tf_h.numpy(), 100.0)       # per-frame TF (config 5 style)
+            ctx.set_lights(li_h.numpy())
+            if world == 1:
+                ctx.render_neural(cam, rc, out=host_frame.numpy())
+            else:
+                step(stats=False)
+                if rank == 0:
+                    host_frame.copy_(frame, non_blocking=True)
+                torch.cuda.synchronize()
+            e_times.append(time.perf_counter() - t0)
+        e_ms = float(np.mean(e_times)) * 1e3
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = tf.nbytes + lights.nbytes + 104 + 128   # TF + lights + camera + render desc
+        e2e = {"value": 1000.0 / e_ms, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(H_ * W_ * 12) if rank == 0 else 0}
+
+    # ---- extras (rank 0): field-query throughput (part c) and KNN gather (config 3)
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = bench_extras(ctx, fc, params, peaks)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            workers = os.cpu_count() or 1
+            rows = 8
+            t = reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam_spec)
+            rows = int(min(H_, max(8, rows * 12.0 / max(t, 1e-3))))
+            t = reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam_spec)
+            cpu = {"value": (rows / H_) / t, "unit": "frames/s", "cores": workers,
+                   "kind": cpu_baseline_kind(),
+                   "sample": f"{rows}/{H_} rows of the same frame ({rows * W_ * SPP} samples), "
+                             f"{t:.1f} s; reference delta_track/transmittance + fp64 field"}
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if args.mode == "fast" else "f64", "data": "synthetic",
+            "config": {"workload": "config 2: 256^3 sphere_sinusoid volume (scene A TF, density 100), "
+                                   "1920x1080, 8 spp, 1 point light, paper photon field "
+                                   "(16x8 hash grid T=2^19, 5x64 MLP, random init)",
+                       "mode": args.mode, "tiles": "16x16 interleaved over ranks",
+                       "l2": "flushed (256 MiB write) between timed frames",
+                       "parallelism": f"tiles{world}"},
+            "mrays_per_s": samples * world / (ms_per_step * 1e-3) / 1e6,
+            "frame": {"samples": samples * world, "hits": hits, "hit_fraction": hits / max(samples, 1),
+                      "steps_per_sample": steps_tot / max(samples, 1),
+                      "ms_trace": tr_ms, "ms_field": fld_ms, "wall_s": wall},
+            "roofline": {"kernel": f"k_render_trace<{args.mode}>", "bound": "hbm",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "per_unit": "32 B (8 x f32 voxels) per tentative collision, "
+                                     f"{steps_tot:.3g} collisions per launch",
+                         "peak_source": peak_kind},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * args.steps + (3 * args.steps if world > 1 else 0),
+            "clocks": clk.summary(),
+            **extras,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_extras(ctx, fc, params, peaks):
+    """Part (c) field-query throughput and the config-3 KNN gather (secondary lines)."""
+    import torch
+    out = {}
+    n = 1 << 22
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.rand((n, 3), device="cuda", generator=g)
+    w = torch.rand((n, 2), device="cuda", generator=g)
+    gg = torch.zeros(n, device="cuda")
+    res = torch.empty((n, 3), device="cuda")
+    for _ in range(3):
+        ctx.field_query(x, w, gg, out=res)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        ctx.field_query(x, w, gg, out=res)
+    b.record()
+    torch.cuda.synchronize()
+    dt = a.elapsed_time(b) / 5 / 1e3
+    din = fc.pos.levels * fc.pos.features + fc.dir.levels * fc.dir.features + 1
+    flop = 2 * (din * 64 + (fc.hidden_layers - 1) * 64 * 64 + 64 * 3)
+    qps = n / dt
+    out["field_query"] = {"queries_per_s": qps, "n": n, "flop_per_query": flop,
+                          "roofline": {"bound": "tensor", "achieved": qps * flop / 1e12,
+                                       "peak": float(peaks["bf16_tflops"]), "unit": "TFLOP/s",
+                                       "frac": qps * flop / 1e12 / float(peaks["bf16_tflops"])},
+                          "gather_bytes_per_query": 2 * (fc.pos.levels * 8 * fc.pos.features +
+                                                         fc.dir.levels * 4 * fc.dir.features)}
+    # config 3: KNN radiance estimate, k = 64 over a 4M-photon 3-phase map
+    from paper_2304_07338_b200.scene import synth_photons
+    ph = synth_photons(4_000_000, 3, seed=3)
+    ph["power"] *= 1e-4
+    ctx.knn_build(ph, [-0.75, 0.0, 0.75])
+    batch = 1 << 16
+    for _ in range(2):
+        ctx.make_batch(seed=1, step=0, batch=batch, K=64)
+    t0 = time.perf_counter()
+    steps = 5
+    for s in range(steps):
+        ctx.make_batch(seed=1, step=s, batch=batch, K=64)
+    dt = (time.perf_counter() - t0) / steps
+    out["knn_gather"] = {"queries_per_s": batch / dt, "batch": batch, "K": 64, "photons": 4_000_000,
+                         "note": "make_batch incl. host copies of the batch; ids bit-exact"}
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

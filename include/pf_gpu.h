@@ -1,0 +1,221 @@
+/*
+ * pf_gpu.h -- C ABI of the B200-native photon-field render hot path.
+ *
+ * The reference (arXiv 2304.07338, /root/reference/proj) is a C++20 library in
+ * namespace pf with no device or process boundary.  This header is the thin
+ * extern "C" layer a drop-in replacement exports so that the reference-side
+ * C++ API (include/pf/gpu.hpp) -- or any FFI (ctypes, cgo, JNI) -- can reach
+ * the sm_100a kernels.  Plain pointers and sizes only; no torch / CUDA types.
+ *
+ * Pointer arguments: every array argument may be a HOST pointer (staged
+ * through the context with cudaMemcpyAsync on the context stream) or a DEVICE
+ * pointer on the context's GPU (used in place).  The kind is detected with
+ * cudaPointerGetAttributes per call.
+ *
+ * Errors: every int-returning entry point returns PF_OK (0),
+ * PF_ERR_INVALID (1, the reference throws std::invalid_argument) or
+ * PF_ERR_RUNTIME (2, std::runtime_error / CUDA / NCCL failure); the message
+ * is in pf_last_error() (thread-local).  include/pf/gpu.hpp rethrows the
+ * matching C++ exception type.
+ *
+ * Randomness: all device randomness is the reference's PCG32
+ * (proj/include/pf/rng.hpp:14-76) with make_rng(seed, stream, index) streams,
+ * so results never depend on launch geometry, tiling or GPU count.
+ */
+#ifndef PF_GPU_H
+#define PF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_ERR_INVALID 1
+#define PF_ERR_RUNTIME 2
+
+/* pf::Stream, proj/include/pf/rng.hpp:62-71 */
+#define PF_STREAM_TRACE 1
+#define PF_STREAM_TRAIN 2
+#define PF_STREAM_CAMERA 3
+#define PF_STREAM_NEE 4
+#define PF_STREAM_PATHTRACE 5
+#define PF_STREAM_FIELDINIT 6
+#define PF_STREAM_SYNTH 7
+#define PF_STREAM_TEST 8
+
+/* Render modes.
+ * PARITY: binary64 delta tracking with the reference's exact operation order
+ *   and RNG consumption; NEE transmittance = nee_trials delta-tracked flights
+ *   exactly as pf::transmittance (proj/src/volume.cpp:227-256).
+ * FAST:   binary32 delta tracking (same streams, 2 x u32 per uniform) and
+ *   ratio-tracked shadow rays with Russian roulette; statistically equal. */
+#define PF_MODE_PARITY 0
+#define PF_MODE_FAST 1
+
+typedef struct pf_ctx pf_ctx;
+
+/* Hash-grid encoding (HashGridConfig). */
+typedef struct {
+    int dims;       /* 3 = position, 2 = direction */
+    int levels;     /* paper 16, desk 8 */
+    int features;   /* paper 8, desk 4 (must be 2, 4 or 8) */
+    int base_res;   /* 4 */
+    double growth;  /* 2.0 */
+    int log2_table; /* paper 19, desk 15 */
+} pf_hashgrid_desc;
+
+/* PhotonField = pos grid + dir grid + MLP. */
+typedef struct {
+    pf_hashgrid_desc pos, dir;
+    int hidden_layers; /* 5 */
+    int width;         /* 64 (the only width the tcgen05 kernel supports) */
+    double psi;        /* Eq. 7/8 precision (5) */
+} pf_field_desc;
+
+/* Pinhole camera: film point (px+u, py+v) maps to
+ * normalize((forward + right*sx) + up*sy), sx = 2(px+u)/W - 1,
+ * sy = 1 - 2(py+v)/H; right/up carry aspect*tan(fov/2) / tan(fov/2). */
+typedef struct {
+    double origin[3];
+    double forward[3];
+    double right[3];
+    double up[3];
+    int width, height;
+} pf_camera;
+
+typedef struct {
+    int spp;               /* samples per pixel, >= 1 */
+    double g;              /* scene phase coefficient */
+    uint64_t seed;         /* config seed: make_rng(seed, CameraSample|Nee, index) */
+    double w_d, w_i;       /* compose weights */
+    double background[3];  /* radiance of samples that never interact */
+    int mode;              /* PF_MODE_PARITY | PF_MODE_FAST */
+    int nee_trials;        /* parity-mode transmittance trials (>= 1) */
+    int use_field;         /* 0: L_i = 0 (direct light only) */
+    int tile_w, tile_h;    /* screen tiles (multi-GPU sharding unit), e.g. 16 x 16 */
+    int shard_index;       /* this rank renders tiles t with t % shard_count == shard_index */
+    int shard_count;       /* 1 on a single GPU */
+} pf_render_desc;
+
+typedef struct {
+    uint64_t samples;        /* camera samples traced */
+    uint64_t hits;           /* samples with a real interaction (= field queries) */
+    uint64_t primary_steps;  /* tentative collisions, primary rays */
+    uint64_t shadow_steps;   /* tentative collisions, shadow rays */
+    float ms_trace, ms_field, ms_compose; /* device time per stage (0 unless timing on) */
+} pf_render_stats;
+
+/* Photon record, pf::Photon (proj/include/pf/photon.hpp:17-22): 40 bytes. */
+typedef struct {
+    float position[3];
+    float direction[3];
+    float power[3];
+    uint8_t g_index;
+    uint8_t pad_[3];
+} pf_photon;
+
+const char *pf_last_error(void);
+const char *pf_version(void);
+
+/* Context on one CUDA device (one process per GPU). */
+int pf_ctx_create(int device, pf_ctx **out);
+void pf_ctx_destroy(pf_ctx *ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL = own stream. */
+int pf_ctx_set_stream(pf_ctx *ctx, void *cuda_stream);
+int pf_ctx_synchronize(pf_ctx *ctx);
+/* Enable per-stage CUDA-event timing inside pf_render_neural. */
+int pf_ctx_set_timing(pf_ctx *ctx, int enabled);
+
+/* ---- scene (replicated per GPU) ----------------------------------------- */
+/* VolumeGrid(nx, ny, nz, data) (volume.hpp:25; validation volume.cpp:24-39):
+ * x-fastest binary32 scalars in [0,1]. */
+int pf_volume_upload(pf_ctx *ctx, int nx, int ny, int nz, const float *data);
+/* Medium(grid, tf, density_scale) (volume.hpp:94): tf_pts = n x (s,r,g,b,a)
+ * with TransferFunction's invariants (volume.cpp:136-149).  sigma_max < 0
+ * computes density_scale * tf.max_alpha(grid range) like volume.cpp:197-202;
+ * otherwise the caller's pf::Medium::sigma_max() is used bit-for-bit. */
+int pf_medium_set(pf_ctx *ctx, const double *tf_pts, int n_pts, double density_scale,
+                  double sigma_max);
+int pf_medium_sigma_max(pf_ctx *ctx, double *out);
+/* LightSource list (photon.hpp:24-27): n x (px,py,pz, Ir,Ig,Ib). */
+int pf_lights_set(pf_ctx *ctx, const double *lights, int n);
+
+/* ---- photon field (part c) ---------------------------------------------- */
+int pf_field_param_count(const pf_field_desc *desc, size_t *out);
+/* Deterministic init from make_rng(seed, FieldInit, 0), drawn in parameter
+ * order: tables U(-embed_scale, embed_scale), weights U(+-sqrt(6/fan_in)),
+ * biases U(-bias_scale, bias_scale).  Host-only helper. */
+int pf_field_init(const pf_field_desc *desc, uint64_t seed, double embed_scale,
+                  double bias_scale, float *params_out);
+/* Flat parameter vector (layout: DESIGN.md "Field parameters"). */
+int pf_field_load(pf_ctx *ctx, const pf_field_desc *desc, const float *params, size_t n);
+/* Batched forward: x3 in [0,1]^3, w_sph2 = (theta/pi,
+ * (phi+pi)/2pi), g raw in [-1,1].  decoded = 0 -> L' (forward), 1 -> radiance
+ * (infer_radiance = decode_log(forward)). */
+int pf_field_query(pf_ctx *ctx, size_t n, const float *x3, const float *w_sph2, const float *g,
+                   float *out_rgb, int decoded);
+
+/* ---- render_neural (Alg. 2) ---------------------------- */
+int pf_camera_make(const double pos[3], const double look_at[3], const double up[3],
+                   double vfov_deg, int width, int height, pf_camera *out);
+/* Renders this shard's tiles into out_rgb (width*height*3 binary32, row-major);
+ * pixels of other shards are left untouched.  stats may be NULL. */
+int pf_render_neural(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
+                     float *out_rgb, pf_render_stats *stats);
+/* Multi-GPU helpers: pack this shard's tiles contiguously (tile order) and
+ * unpack all shards' packed buffers into a frame. */
+int pf_tiles_count(const pf_camera *cam, const pf_render_desc *desc, int shard, int *n_tiles);
+int pf_tiles_pack(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
+                  const float *frame_rgb, float *packed);
+int pf_tiles_unpack(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
+                    const float *packed_all, size_t per_shard_floats, float *frame_rgb);
+
+/* ---- parity entry points: batched pf::delta_track / pf::transmittance --- */
+/* Ray i: origin o3[3i..], unit direction d3[3i..], [tmin, tmax]; its RNG is
+ * make_rng(seed, stream, idx[i]).  hit[i] = 1/0, pos3 / rgba4 (may be NULL)
+ * receive Interaction::position / albedo.  fp64 = 1: binary64 parity kernel;
+ * 0: binary32 fast kernel.  Invalid rays -> PF_ERR_INVALID (volume.cpp:205-207). */
+int pf_delta_track_batch(pf_ctx *ctx, size_t n, const double *o3, const double *d3,
+                         const double *tmin, const double *tmax, uint64_t seed, uint64_t stream,
+                         const uint64_t *idx, int fp64, int *hit, double *pos3, double *rgba4);
+/* transmittance(medium, a, b, rng, n_trials) per segment (binary64). */
+int pf_transmittance_batch(pf_ctx *ctx, size_t n, const double *a3, const double *b3,
+                           uint64_t seed, uint64_t stream, const uint64_t *idx, int n_trials,
+                           double *out);
+/* Ratio-tracking transmittance (fast mode estimator, binary32): unbiased
+ * estimate of the same quantity; n_trials estimates averaged. */
+int pf_transmittance_ratio_batch(pf_ctx *ctx, size_t n, const double *a3, const double *b3,
+                                 uint64_t seed, uint64_t stream, const uint64_t *idx,
+                                 int n_trials, double *out);
+/* Device PCG32: draws next_double() n_draws times from make_rng(seed,
+ * stream, idx[i]) into out[i*n_draws + k] (rng.hpp:41). */
+int pf_rng_doubles(pf_ctx *ctx, size_t n, uint64_t seed, uint64_t stream, const uint64_t *idx,
+                   int n_draws, double *out);
+
+/* ---- photon map + KNN training-target gather (config 3) ----------------- */
+/* build(photons): per-phase cell grid, ids = load order. */
+int pf_knn_build(pf_ctx *ctx, const pf_photon *photons, size_t n, int n_phases,
+                 const double *phase_set);
+/* knn_phase: exact min(K, m) nearest photons of tag gidx[i]
+ * with d2 <= r_max^2, ascending (d2, id); ids/d2 are nq x K (unused slots:
+ * id 0xFFFFFFFF, d2 +inf); counts[i] = min(K, m).  Bit-exact with the oracle. */
+int pf_knn_query(pf_ctx *ctx, size_t nq, const float *x3, const uint8_t *gidx, int K,
+                 float r_max, uint32_t *ids, float *d2, int32_t *counts);
+/* make_batch target gather: KNN -> Eq. 6 (binary64) -> Eq. 7, out3 = log
+ * targets in [0,1] (binary64).  ids/d2/counts may be NULL. */
+int pf_knn_targets(pf_ctx *ctx, size_t nq, const float *x3, const double *w3,
+                   const uint8_t *gidx, int K, float r_max, double psi, double *out3,
+                   uint32_t *ids, float *d2, int32_t *counts);
+/* Whole make_batch on device: queries from
+ * make_rng(seed, Train, step*batch + i) (x ~ U^3 as f32, w ~ uniform sphere,
+ * g ~ next_below(n_phases)), then the target gather. */
+int pf_make_batch(pf_ctx *ctx, uint64_t seed, uint64_t step, size_t batch, int K, float r_max,
+                  double psi, float *x3, double *w3, uint8_t *gidx, double *targets3);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_GPU_H */

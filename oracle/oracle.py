@@ -1,0 +1,423 @@
+"""ctypes wrapper of the CPU ORACLE (TEST INFRASTRUCTURE ONLY).
+
+Loaded only by tests/, __graft_entry__.smoke() (as the checker) and bench.py's
+cpu_baseline / --impl reference leg.  Two libraries:
+  oracle/liboracle.so     -- the C restatement (pf_oracle.c), always buildable
+  oracle/_ref/libpfref.so -- the UNMODIFIED reference sources + ref_shim.cpp;
+                             built here only when /root/reference exists, then
+                             shipped prebuilt (it is git-ignored, not gpurun-ignored)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libpfref.so"
+REF_SRC = Path(os.environ.get("PF_REFERENCE", "/root/reference"))
+
+
+def build(ref: bool | None = None) -> None:
+    """make -C oracle (the C restatement; + _ref when the reference is present)."""
+    targets = [str(LIB)]
+    if ref is None:
+        ref = (REF_SRC / "proj" / "src" / "volume.cpp").exists()
+    if ref:
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", str(HERE), f"REF={REF_SRC}", *targets], check=True,
+                   capture_output=True)
+
+
+class Grid(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("data", C.c_void_p),
+                ("value_min", C.c_float), ("value_max", C.c_float)]
+
+
+class Tf(C.Structure):
+    _fields_ = [("n", C.c_int), ("pts", C.c_void_p)]
+
+
+class Medium(C.Structure):
+    _fields_ = [("grid", Grid), ("tf", Tf), ("density_scale", C.c_double),
+                ("sigma_max", C.c_double)]
+
+
+class HashCfg(C.Structure):
+    _fields_ = [("dims", C.c_int), ("levels", C.c_int), ("features", C.c_int),
+                ("base_res", C.c_int), ("growth", C.c_double), ("log2_table", C.c_int)]
+
+
+class FieldCfg(C.Structure):
+    _fields_ = [("pos", HashCfg), ("dir", HashCfg), ("hidden_layers", C.c_int), ("width", C.c_int),
+                ("psi", C.c_double)]
+
+
+class Camera(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("forward", C.c_double * 3), ("right", C.c_double * 3),
+                ("up", C.c_double * 3), ("width", C.c_int), ("height", C.c_int)]
+
+
+class Light(C.Structure):
+    _fields_ = [("pos", C.c_double * 3), ("intensity", C.c_double * 3)]
+
+
+class RenderCfg(C.Structure):
+    _fields_ = [("spp", C.c_int), ("g", C.c_double), ("seed", C.c_uint64), ("w_d", C.c_double),
+                ("w_i", C.c_double), ("background", C.c_double * 3), ("nee_trials", C.c_int),
+                ("use_field", C.c_int), ("x0", C.c_int), ("y0", C.c_int), ("x1", C.c_int),
+                ("y1", C.c_int)]
+
+
+class RenderStats(C.Structure):
+    _fields_ = [("samples", C.c_uint64), ("hits", C.c_uint64)]
+
+
+_P = C.c_void_p
+_SIG = {
+    "or_next_u32": (C.c_uint32, [_P]),
+    "or_next_double": (C.c_double, [_P]),
+    "or_make_rng": (None, [_P, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "or_splitmix64": (C.c_uint64, [C.c_uint64]),
+    "or_hg_eval": (C.c_double, [C.c_double, C.c_double]),
+    "or_aabb_intersect": (C.c_int, [_P, _P, C.c_double, C.c_double, _P, _P]),
+    "or_grid_init": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P]),
+    "or_grid_sample": (C.c_double, [_P, _P]),
+    "or_tf_classify": (None, [_P, C.c_double, _P]),
+    "or_medium_init": (C.c_int, [_P, _P, _P, C.c_double]),
+    "or_delta_track_batch": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_uint64, C.c_uint64, _P,
+                                       _P, _P, _P]),
+    "or_transmittance_batch": (None, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64, _P, C.c_int,
+                                      _P]),
+    "or_rng_doubles": (None, [C.c_uint64, C.c_uint64, C.c_size_t, _P, C.c_int, _P]),
+    "or_field_param_count": (C.c_size_t, [_P]),
+    "or_field_input_dim": (C.c_int, [_P]),
+    "or_field_encode": (None, [_P, _P, _P, _P, C.c_double, _P]),
+    "or_field_forward": (None, [_P, _P, C.c_size_t, _P, _P, _P, _P]),
+    "or_field_infer": (None, [_P, _P, C.c_size_t, _P, _P, _P, _P]),
+    "or_dir_to_sph": (None, [_P, _P]),
+    "or_encode_log": (C.c_double, [C.c_double, C.c_double]),
+    "or_decode_log": (C.c_double, [C.c_double, C.c_double]),
+    "or_knn_brute": (C.c_int, [_P, C.c_size_t, _P, C.c_int, C.c_int, C.c_float, _P, _P]),
+    "or_kd_build": (C.c_void_p, [_P, C.c_size_t]),
+    "or_kd_free": (None, [_P]),
+    "or_kd_knn": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_float, _P, _P]),
+    "or_estimate_radiance": (None, [_P, _P, _P, C.c_int, _P, C.c_double, _P]),
+    "or_make_queries": (None, [C.c_uint64, C.c_uint64, C.c_size_t, C.c_int, _P, _P, _P]),
+    "or_schedule_radius": (C.c_double, [_P, _P, C.c_int, C.c_uint64, C.c_uint64]),
+    "or_knn_targets": (None, [_P, _P, C.c_size_t, _P, _P, _P, _P, C.c_int, C.c_float, C.c_double,
+                              _P, _P, _P, _P]),
+    "or_camera_make": (None, [_P, _P, _P, _P, C.c_double, C.c_int, C.c_int]),
+    "or_render_neural": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P]),
+}
+
+_REF_SIG = {
+    "ref_last_error": (C.c_char_p, []),
+    "ref_rng_u32": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _P]),
+    "ref_rng_double": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _P]),
+    "ref_splitmix64": (C.c_uint64, [C.c_uint64]),
+    "ref_hg_eval": (C.c_double, [C.c_double, C.c_double]),
+    "ref_hg_sample_cos": (C.c_double, [C.c_double, C.c_double]),
+    "ref_hg_cdf": (C.c_double, [C.c_double, C.c_double]),
+    "ref_hg_sample": (None, [C.c_double, _P, C.c_double, C.c_double, _P]),
+    "ref_aabb_intersect": (C.c_int, [_P, _P, C.c_double, C.c_double, _P, _P]),
+    "ref_scene_create": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, _P, C.c_int, C.c_double,
+                                   C.POINTER(C.c_void_p)]),
+    "ref_scene_destroy": (None, [_P]),
+    "ref_scene_sigma_max": (C.c_double, [_P]),
+    "ref_grid_sample": (C.c_double, [_P, _P]),
+    "ref_tf_classify": (None, [_P, C.c_double, _P]),
+    "ref_delta_track_batch": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_uint64, C.c_uint64,
+                                        _P, _P, _P, _P]),
+    "ref_transmittance_batch": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64, _P,
+                                          C.c_int, _P]),
+    "ref_render_neural": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P]),
+}
+
+_lib = None
+_ref = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            build(ref=False)
+        L = C.CDLL(str(LIB))
+        for k, (r, a) in _SIG.items():
+            f = getattr(L, k)
+            f.restype, f.argtypes = r, a
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return REF_LIB.exists() or (REF_SRC / "proj" / "src" / "volume.cpp").exists()
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not REF_LIB.exists():
+            build(ref=True)
+        L = C.CDLL(str(REF_LIB))
+        for k, (r, a) in _REF_SIG.items():
+            f = getattr(L, k)
+            f.restype, f.argtypes = r, a
+        _ref = L
+    return _ref
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ------------------------------------------------------------ scene ------
+
+
+class OracleScene:
+    """A medium (grid + TF + density) for the C restatement."""
+
+    def __init__(self, vol: np.ndarray, tf: np.ndarray, density_scale: float = 100.0):
+        self.vol = np.ascontiguousarray(vol, dtype=np.float32)
+        self.tf = np.ascontiguousarray(tf, dtype=np.float64)
+        nz, ny, nx = self.vol.shape
+        self.grid = Grid()
+        if lib().or_grid_init(C.byref(self.grid), nx, ny, nz, _p(self.vol)):
+            raise ValueError("VolumeGrid: invalid")
+        self.tfs = Tf(self.tf.shape[0], _p(self.tf))
+        self.medium = Medium()
+        if lib().or_medium_init(C.byref(self.medium), C.byref(self.grid), C.byref(self.tfs),
+                                density_scale):
+            raise ValueError("Medium: invalid density scale")
+
+    @property
+    def sigma_max(self) -> float:
+        return self.medium.sigma_max
+
+    def delta_track(self, o, d, tmin, tmax, seed, stream, idx):
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        tmin = np.ascontiguousarray(tmin, np.float64)
+        tmax = np.ascontiguousarray(tmax, np.float64)
+        idx = np.ascontiguousarray(idx, np.uint64)
+        n = len(idx)
+        hit = np.zeros(n, np.int32)
+        pos = np.zeros((n, 3))
+        rgba = np.zeros((n, 4))
+        if lib().or_delta_track_batch(C.byref(self.medium), n, _p(o), _p(d), _p(tmin), _p(tmax),
+                                      seed, stream, _p(idx), _p(hit), _p(pos), _p(rgba)):
+            raise ValueError("delta_track: invalid ray")
+        return hit, pos, rgba
+
+    def transmittance(self, a, b, seed, stream, idx, n_trials=1):
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        idx = np.ascontiguousarray(idx, np.uint64)
+        out = np.zeros(len(idx))
+        lib().or_transmittance_batch(C.byref(self.medium), len(idx), _p(a), _p(b), seed, stream,
+                                     _p(idx), n_trials, _p(out))
+        return out
+
+    def sample(self, p) -> float:
+        p = np.ascontiguousarray(p, np.float64)
+        return lib().or_grid_sample(C.byref(self.grid), _p(p))
+
+
+class RefScene:
+    """The same medium through the UNMODIFIED reference (oracle/_ref)."""
+
+    def __init__(self, vol: np.ndarray, tf: np.ndarray, density_scale: float = 100.0):
+        self.vol = np.ascontiguousarray(vol, dtype=np.float32)
+        self.tf = np.ascontiguousarray(tf, dtype=np.float64)
+        nz, ny, nx = self.vol.shape
+        h = C.c_void_p()
+        if ref().ref_scene_create(nx, ny, nz, _p(self.vol), _p(self.tf), self.tf.shape[0],
+                                  density_scale, C.byref(h)):
+            raise ValueError(ref().ref_last_error().decode())
+        self.h = h
+
+    def __del__(self):
+        try:
+            ref().ref_scene_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def sigma_max(self) -> float:
+        return ref().ref_scene_sigma_max(self.h)
+
+    def delta_track(self, o, d, tmin, tmax, seed, stream, idx):
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        tmin = np.ascontiguousarray(tmin, np.float64)
+        tmax = np.ascontiguousarray(tmax, np.float64)
+        idx = np.ascontiguousarray(idx, np.uint64)
+        n = len(idx)
+        hit = np.zeros(n, np.int32)
+        pos = np.zeros((n, 3))
+        rgba = np.zeros((n, 4))
+        if ref().ref_delta_track_batch(self.h, n, _p(o), _p(d), _p(tmin), _p(tmax), seed, stream,
+                                       _p(idx), _p(hit), _p(pos), _p(rgba)):
+            raise ValueError(ref().ref_last_error().decode())
+        return hit, pos, rgba
+
+    def transmittance(self, a, b, seed, stream, idx, n_trials=1):
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        idx = np.ascontiguousarray(idx, np.uint64)
+        out = np.zeros(len(idx))
+        if ref().ref_transmittance_batch(self.h, len(idx), _p(a), _p(b), seed, stream, _p(idx),
+                                         n_trials, _p(out)):
+            raise ValueError(ref().ref_last_error().decode())
+        return out
+
+
+# ------------------------------------------------------------ field ------
+
+
+def field_cfg(fc) -> FieldCfg:
+    """From paper_2304_07338_b200.FieldConfig (duck-typed)."""
+    def h(g):
+        return HashCfg(g.dims, g.levels, g.features, g.base_res, float(g.growth), g.log2_table)
+    return FieldCfg(h(fc.pos), h(fc.dir), fc.hidden_layers, fc.width, float(fc.psi))
+
+
+def field_param_count(fc) -> int:
+    return lib().or_field_param_count(C.byref(field_cfg(fc)))
+
+
+def field_forward(fc, params, x3, w2, g, decoded=False) -> np.ndarray:
+    cfg = field_cfg(fc)
+    params = np.ascontiguousarray(params, np.float32)
+    x3 = np.ascontiguousarray(x3, np.float64)
+    w2 = np.ascontiguousarray(w2, np.float64)
+    g = np.ascontiguousarray(g, np.float64)
+    out = np.zeros((len(g), 3))
+    fn = lib().or_field_infer if decoded else lib().or_field_forward
+    fn(C.byref(cfg), _p(params), len(g), _p(x3), _p(w2), _p(g), _p(out))
+    return out
+
+
+def field_encode(fc, params, x, w, g) -> np.ndarray:
+    cfg = field_cfg(fc)
+    params = np.ascontiguousarray(params, np.float32)
+    x = np.ascontiguousarray(x, np.float64)
+    w = np.ascontiguousarray(w, np.float64)
+    out = np.zeros(lib().or_field_input_dim(C.byref(cfg)))
+    lib().or_field_encode(C.byref(cfg), _p(params), _p(x), _p(w), float(g), _p(out))
+    return out
+
+
+# -------------------------------------------------------------- KNN ------
+
+
+class KdTree:
+    def __init__(self, photons: np.ndarray):
+        self.ph = np.ascontiguousarray(photons)
+        assert self.ph.dtype.itemsize == 40
+        self.t = lib().or_kd_build(_p(self.ph), len(self.ph))
+
+    def __del__(self):
+        try:
+            lib().or_kd_free(self.t)
+        except Exception:
+            pass
+
+    def knn(self, q, g_index, K, r_max=float("inf")):
+        q = np.ascontiguousarray(q, np.float32)
+        ids = np.zeros(K, np.uint32)
+        d2 = np.zeros(K, np.float32)
+        n = lib().or_kd_knn(self.t, _p(q), g_index, K, r_max, _p(ids), _p(d2))
+        return ids[:n], d2[:n]
+
+    def targets(self, x3, w3, gidx, phase_set, K, r_max, psi):
+        x3 = np.ascontiguousarray(x3, np.float32)
+        w3 = np.ascontiguousarray(w3, np.float64)
+        gidx = np.ascontiguousarray(gidx, np.uint8)
+        ps = np.ascontiguousarray(phase_set, np.float64)
+        n = len(gidx)
+        ids = np.zeros((n, K), np.uint32)
+        d2 = np.zeros((n, K), np.float32)
+        cnt = np.zeros(n, np.int32)
+        tg = np.zeros((n, 3))
+        lib().or_knn_targets(self.t, _p(self.ph), n, _p(x3), _p(w3), _p(gidx), _p(ps), K, r_max,
+                             psi, _p(ids), _p(d2), _p(cnt), _p(tg))
+        return tg, ids, d2, cnt
+
+
+def knn_brute(photons, q, g_index, K, r_max=float("inf")):
+    ph = np.ascontiguousarray(photons)
+    q = np.ascontiguousarray(q, np.float32)
+    ids = np.zeros(K, np.uint32)
+    d2 = np.zeros(K, np.float32)
+    n = lib().or_knn_brute(_p(ph), len(ph), _p(q), g_index, K, r_max, _p(ids), _p(d2))
+    return ids[:n], d2[:n]
+
+
+def make_queries(seed, step, batch, n_phases):
+    x = np.zeros((batch, 3), np.float32)
+    w = np.zeros((batch, 3))
+    g = np.zeros(batch, np.uint8)
+    lib().or_make_queries(seed, step, batch, n_phases, _p(x), _p(w), _p(g))
+    return x, w, g
+
+
+# ----------------------------------------------------------- render ------
+
+
+def camera(spec) -> Camera:
+    cam = Camera()
+    pos = np.array(spec.position, np.float64)
+    at = np.array(spec.look_at, np.float64)
+    up = np.array(spec.up, np.float64)
+    lib().or_camera_make(C.byref(cam), _p(pos), _p(at), _p(up), float(spec.vfov_deg), spec.width,
+                         spec.height)
+    return cam
+
+
+def _lights(lights: np.ndarray):
+    arr = (Light * len(lights))()
+    for i, l in enumerate(lights):
+        arr[i].pos[:] = list(l[:3])
+        arr[i].intensity[:] = list(l[3:6])
+    return arr
+
+
+def _rcfg(rc, cam, rect):
+    x0, y0, x1, y1 = rect if rect is not None else (0, 0, cam.width, cam.height)
+    return RenderCfg(rc.spp, float(rc.g), rc.seed, float(rc.w_d), float(rc.w_i),
+                     (C.c_double * 3)(*rc.background), rc.nee_trials, int(rc.use_field), x0, y0,
+                     x1, y1)
+
+
+def render_neural(scene: OracleScene, lights, fc, params, cam_spec, rc, rect=None):
+    """The C restatement of render_neural (binary64; returns (H, W, 3) float32)."""
+    cam = camera(cam_spec)
+    ls = _lights(np.asarray(lights, np.float64).reshape(-1, 6))
+    cfg = field_cfg(fc) if fc is not None else FieldCfg()
+    params = np.ascontiguousarray(params if params is not None else np.zeros(1), np.float32)
+    out = np.zeros((cam.height, cam.width, 3), np.float32)
+    st = RenderStats()
+    lib().or_render_neural(C.byref(scene.medium), ls, len(ls), C.byref(cfg), _p(params),
+                           C.byref(cam), C.byref(_rcfg(rc, cam, rect)), _p(out), C.byref(st))
+    return out, {"samples": st.samples, "hits": st.hits}
+
+
+def ref_render_neural(scene: RefScene, lights, fc, params, cam_spec, rc, rect=None, workers=0):
+    """The reference CPU path (pf::delta_track/transmittance + parallel_chunks)."""
+    cam = camera(cam_spec)
+    ls = _lights(np.asarray(lights, np.float64).reshape(-1, 6))
+    cfg = field_cfg(fc) if fc is not None else FieldCfg()
+    params = np.ascontiguousarray(params if params is not None else np.zeros(1), np.float32)
+    out = np.zeros((cam.height, cam.width, 3), np.float32)
+    hits = C.c_uint64()
+    if ref().ref_render_neural(scene.h, ls, len(ls), C.byref(cfg), _p(params), C.byref(cam),
+                               C.byref(_rcfg(rc, cam, rect)), workers or (os.cpu_count() or 1),
+                               _p(out), C.byref(hits)):
+        raise ValueError(ref().ref_last_error().decode())
+    return out, {"hits": hits.value}

@@ -1,0 +1,347 @@
+"""Python mirror of the reference's pf:: render-path API over the C ABI.
+
+Reference interface (namespace pf, /root/reference/proj + SPEC.md) -> here:
+  pf::Medium(grid, tf, density_scale)        Context.upload_volume + set_medium
+  pf::delta_track(medium, ray, rng)          Context.delta_track_batch
+  pf::transmittance(medium, a, b, rng, n)    Context.transmittance_batch
+  pf::make_rng(seed, stream, index)          Context.rng_doubles (device PCG32)
+  render_neural(scene, field, cfg, cam, spp) Context.render_neural
+  forward / infer_radiance                   Context.field_query
+  build / knn_phase                          Context.knn_build / knn_query
+  Eq.6 + Eq.7 target gather, make_batch      Context.knn_targets / make_batch
+Errors: ValueError where the reference throws std::invalid_argument,
+RuntimeError for std::runtime_error / CUDA failures.
+
+Array arguments may be numpy arrays (host; staged by the library) or CUDA
+torch tensors (device; used in place, results stay on the device).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _lib
+from ._lib import STREAM, check, lib
+from .scene import PHOTON_DTYPE, CameraSpec, validate_tf
+
+# ------------------------------------------------------------ configs -----
+
+
+@dataclass
+class HashGrid:
+    dims: int
+    levels: int
+    features: int
+    base_res: int = 4
+    growth: float = 2.0
+    log2_table: int = 15
+
+    def c(self) -> _lib.HashGridDesc:
+        return _lib.HashGridDesc(self.dims, self.levels, self.features, self.base_res,
+                                 float(self.growth), self.log2_table)
+
+
+@dataclass
+class FieldConfig:
+    """PhotonField = pos hash grid + dir hash grid + MLP."""
+    pos: HashGrid = field(default_factory=lambda: HashGrid(3, 8, 4))
+    dir: HashGrid = field(default_factory=lambda: HashGrid(2, 8, 4))
+    hidden_layers: int = 5
+    width: int = 64
+    psi: float = 5.0
+
+    @staticmethod
+    def desk() -> "FieldConfig":
+        """SPEC.md:434 desk scale: 8 levels x 4 features, T = 2^15."""
+        return FieldConfig()
+
+    @staticmethod
+    def paper() -> "FieldConfig":
+        """PAPER.md:351 / SPEC.md:358: 16 levels x 8 features, T = 2^19, growth 2."""
+        return FieldConfig(HashGrid(3, 16, 8, 4, 2.0, 19), HashGrid(2, 16, 8, 4, 2.0, 19))
+
+    def c(self) -> _lib.FieldDesc:
+        return _lib.FieldDesc(self.pos.c(), self.dir.c(), self.hidden_layers, self.width,
+                              float(self.psi))
+
+    def param_count(self) -> int:
+        n = C.c_size_t()
+        check(lib().pf_field_param_count(C.byref(self.c()), C.byref(n)))
+        return n.value
+
+    def init_params(self, seed: int = 0, embed_scale: float = 1e-4,
+                    bias_scale: float = 0.0) -> np.ndarray:
+        """Deterministic init from make_rng(seed, FieldInit, 0)."""
+        out = np.empty(self.param_count(), dtype=np.float32)
+        check(lib().pf_field_init(C.byref(self.c()), seed, embed_scale, bias_scale,
+                                  out.ctypes.data))
+        return out
+
+
+@dataclass
+class RenderConfig:
+    spp: int = 1
+    g: float = 0.0
+    seed: int = 0
+    w_d: float = 1.0
+    w_i: float = 1.0
+    background: tuple = (0.0, 0.0, 0.0)
+    mode: str = "fast"            # "parity" (binary64, delta-trial NEE) | "fast"
+    nee_trials: int = 1
+    use_field: bool = True
+    tile: tuple = (16, 16)
+    shard_index: int = 0
+    shard_count: int = 1
+
+    def c(self) -> _lib.RenderDesc:
+        mode = {"parity": _lib.PF_MODE_PARITY, "fast": _lib.PF_MODE_FAST}[self.mode]
+        return _lib.RenderDesc(self.spp, float(self.g), self.seed, float(self.w_d),
+                               float(self.w_i), (C.c_double * 3)(*self.background), mode,
+                               self.nee_trials, int(self.use_field), self.tile[0], self.tile[1],
+                               self.shard_index, self.shard_count)
+
+
+# ------------------------------------------------------------- helpers ----
+
+
+def _is_torch(x: Any) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _in(x: Any, dtype, shape_tail=None) -> tuple[int, Any]:
+    """(pointer, keepalive) for an input array."""
+    if _is_torch(x):
+        if not x.is_contiguous():
+            x = x.contiguous()
+        return x.data_ptr(), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    if shape_tail is not None and a.shape[1:] != shape_tail:
+        a = a.reshape((-1,) + shape_tail)
+    return a.ctypes.data, a
+
+
+def _out(out: Any, shape, dtype) -> tuple[int, Any]:
+    if out is None:
+        out = np.empty(shape, dtype=dtype)
+    if _is_torch(out):
+        return out.data_ptr(), out
+    return out.ctypes.data, out
+
+
+def _n(x: Any) -> int:
+    return int(x.shape[0])
+
+
+# ------------------------------------------------------------- context ----
+
+
+class Context:
+    """One CUDA device; scene, field and photon map are device-resident."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = C.c_void_p()
+        check(lib().pf_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.field_config: FieldConfig | None = None
+        if stream is not None:
+            self.set_stream(stream)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().pf_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_stream(self, cuda_stream: int | None) -> None:
+        check(lib().pf_ctx_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
+
+    def synchronize(self) -> None:
+        check(lib().pf_ctx_synchronize(self._h))
+
+    def set_timing(self, on: bool) -> None:
+        check(lib().pf_ctx_set_timing(self._h, int(on)))
+
+    # ---- scene
+    def upload_volume(self, v) -> None:
+        """VolumeGrid(nx, ny, nz, data): v has shape (nz, ny, nx), x fastest."""
+        p, keep = _in(v, np.float32)
+        nz, ny, nx = keep.shape
+        check(lib().pf_volume_upload(self._h, nx, ny, nz, p))
+
+    def set_medium(self, tf_points, density_scale: float = 100.0,
+                   sigma_max: float = -1.0) -> float:
+        tf = validate_tf(tf_points)
+        check(lib().pf_medium_set(self._h, tf.ctypes.data, tf.shape[0], float(density_scale),
+                                  float(sigma_max)))
+        return self.sigma_max
+
+    @property
+    def sigma_max(self) -> float:
+        v = C.c_double()
+        check(lib().pf_medium_sigma_max(self._h, C.byref(v)))
+        return v.value
+
+    def set_lights(self, lights) -> None:
+        a = np.ascontiguousarray(lights, dtype=np.float64).reshape(-1, 6)
+        check(lib().pf_lights_set(self._h, a.ctypes.data, a.shape[0]))
+
+    # ---- field
+    def load_field(self, cfg: FieldConfig, params) -> None:
+        p, keep = _in(params, np.float32)
+        check(lib().pf_field_load(self._h, C.byref(cfg.c()), p, int(np.prod(keep.shape))))
+        self.field_config = cfg
+
+    def field_query(self, x3, wsph2, g, decoded: bool = True, out=None):
+        px, kx = _in(x3, np.float32)
+        pw, kw = _in(wsph2, np.float32)
+        pg, kg = _in(g, np.float32)
+        n = _n(kx)
+        po, out = _out(out, (n, 3), np.float32)
+        check(lib().pf_field_query(self._h, n, px, pw, pg, po, int(decoded)))
+        return out
+
+    # ---- render
+    @staticmethod
+    def camera(spec: CameraSpec) -> _lib.Camera:
+        cam = _lib.Camera()
+        pos = (C.c_double * 3)(*spec.position)
+        at = (C.c_double * 3)(*spec.look_at)
+        up = (C.c_double * 3)(*spec.up)
+        check(lib().pf_camera_make(pos, at, up, float(spec.vfov_deg), spec.width, spec.height,
+                                   C.byref(cam)))
+        return cam
+
+    def render_neural(self, cam: _lib.Camera | CameraSpec, cfg: RenderConfig, out=None,
+                      stats: bool = False):
+        if isinstance(cam, CameraSpec):
+            cam = self.camera(cam)
+        po, out = _out(out, (cam.height, cam.width, 3), np.float32)
+        st = _lib.RenderStats()
+        check(lib().pf_render_neural(self._h, C.byref(cam), C.byref(cfg.c()), po,
+                                     C.byref(st) if stats else None))
+        if stats:
+            return out, {k: getattr(st, k) for k, _ in _lib.RenderStats._fields_}
+        return out
+
+    def tiles_count(self, cam: _lib.Camera, cfg: RenderConfig, shard: int) -> int:
+        n = C.c_int()
+        check(lib().pf_tiles_count(C.byref(cam), C.byref(cfg.c()), shard, C.byref(n)))
+        return n.value
+
+    def tiles_pack(self, cam, cfg: RenderConfig, frame, packed) -> None:
+        check(lib().pf_tiles_pack(self._h, C.byref(cam), C.byref(cfg.c()), frame.data_ptr(),
+                                  packed.data_ptr()))
+
+    def tiles_unpack(self, cam, cfg: RenderConfig, packed_all, per_shard: int, frame) -> None:
+        check(lib().pf_tiles_unpack(self._h, C.byref(cam), C.byref(cfg.c()),
+                                    packed_all.data_ptr(), per_shard, frame.data_ptr()))
+
+    # ---- parity entry points
+    def delta_track_batch(self, o3, d3, tmin, tmax, seed: int, stream: str | int, idx,
+                          fp64: bool = True):
+        po, ko = _in(o3, np.float64)
+        pd, kd = _in(d3, np.float64)
+        p0, k0 = _in(tmin, np.float64)
+        p1, k1 = _in(tmax, np.float64)
+        pi, ki = _in(idx, np.uint64)
+        n = _n(ko)
+        ph, hit = _out(None, (n,), np.int32)
+        pp, pos = _out(None, (n, 3), np.float64)
+        pr, rgba = _out(None, (n, 4), np.float64)
+        s = STREAM[stream] if isinstance(stream, str) else int(stream)
+        check(lib().pf_delta_track_batch(self._h, n, po, pd, p0, p1, seed, s, pi, int(fp64), ph,
+                                         pp, pr))
+        return hit, pos, rgba
+
+    def transmittance_batch(self, a3, b3, seed: int, stream: str | int, idx, n_trials: int = 1,
+                            ratio: bool = False):
+        pa, ka = _in(a3, np.float64)
+        pb, kb = _in(b3, np.float64)
+        pi, ki = _in(idx, np.uint64)
+        n = _n(ka)
+        po, out = _out(None, (n,), np.float64)
+        s = STREAM[stream] if isinstance(stream, str) else int(stream)
+        fn = lib().pf_transmittance_ratio_batch if ratio else lib().pf_transmittance_batch
+        check(fn(self._h, n, pa, pb, seed, s, pi, n_trials, po))
+        return out
+
+    def rng_doubles(self, seed: int, stream: str | int, idx, n_draws: int):
+        pi, ki = _in(idx, np.uint64)
+        n = _n(ki)
+        po, out = _out(None, (n, n_draws), np.float64)
+        s = STREAM[stream] if isinstance(stream, str) else int(stream)
+        check(lib().pf_rng_doubles(self._h, n, seed, s, pi, n_draws, po))
+        return out
+
+    # ---- photon map / KNN
+    def knn_build(self, photons, phase_set) -> None:
+        if _is_torch(photons):
+            n = photons.numel() // 40
+            p, keep = photons.data_ptr(), photons
+        else:
+            a = np.ascontiguousarray(photons, dtype=PHOTON_DTYPE)
+            n, p, keep = len(a), a.ctypes.data, a
+        ps = np.ascontiguousarray(phase_set, dtype=np.float64)
+        check(lib().pf_knn_build(self._h, p, n, len(ps), ps.ctypes.data))
+        self.phase_set = ps
+
+    def knn_query(self, x3, gidx, K: int, r_max: float = float("inf")):
+        px, kx = _in(x3, np.float32)
+        pg, kg = _in(gidx, np.uint8)
+        n = _n(kx)
+        pi, ids = _out(None, (n, K), np.uint32)
+        pd, d2 = _out(None, (n, K), np.float32)
+        pc, cnt = _out(None, (n,), np.int32)
+        check(lib().pf_knn_query(self._h, n, px, pg, K, float(r_max), pi, pd, pc))
+        return ids, d2, cnt
+
+    def knn_targets(self, x3, w3, gidx, K: int, r_max: float = float("inf"), psi: float = 5.0,
+                    with_ids: bool = False):
+        px, kx = _in(x3, np.float32)
+        pw, kw = _in(w3, np.float64)
+        pg, kg = _in(gidx, np.uint8)
+        n = _n(kx)
+        pt, tg = _out(None, (n, 3), np.float64)
+        if with_ids:
+            pi, ids = _out(None, (n, K), np.uint32)
+            pd, d2 = _out(None, (n, K), np.float32)
+            pc, cnt = _out(None, (n,), np.int32)
+        else:
+            pi = pd = pc = None
+        check(lib().pf_knn_targets(self._h, n, px, pw, pg, K, float(r_max), float(psi), pt, pi,
+                                   pd, pc))
+        return (tg, ids, d2, cnt) if with_ids else tg
+
+    def make_batch(self, seed: int, step: int, batch: int, K: int,
+                   r_max: float = float("inf"), psi: float = 5.0):
+        px, x = _out(None, (batch, 3), np.float32)
+        pw, w = _out(None, (batch, 3), np.float64)
+        pg, g = _out(None, (batch,), np.uint8)
+        pt, t = _out(None, (batch, 3), np.float64)
+        check(lib().pf_make_batch(self._h, seed, step, batch, K, float(r_max), float(psi), px,
+                                  pw, pg, pt))
+        return x, w, g, t
+
+
+def schedule_radius(ends, radii, step: int, total: int) -> float:
+    """KnnSchedule lookup: first segment whose end >= (step+1)/total."""
+    progress = (step + 1) / total
+    for e, r in zip(ends, radii):
+        if e >= progress:
+            return float(r)
+    return float(radii[-1])

@@ -1,0 +1,110 @@
+// pf_compose.cu -- K5 compose + multi-GPU tile pack/unpack.
+//
+// compose (Alg. 2):
+//   L(pixel) = (1/spp) * sum_{k=0..spp-1} slot_k
+// where slot_k already holds w_d*L_d,k + w_i*sigma_s,k*L_i,k (or the
+// background for samples that never interact).  The sum runs in sample order
+// k = 0..spp-1 (binary64 in parity mode), exactly like the oracle, so the
+// frame is deterministic and independent of the tile/GPU partition.
+#include "pf_kernels.h"
+
+namespace pfk {
+
+__device__ __forceinline__ bool tile_pixel(const ComposeParams &C, uint32_t lt, uint32_t pix,
+                                           int &px, int &py) {
+    const uint32_t t = lt * (uint32_t)C.shard_count + (uint32_t)C.shard_index;
+    const uint32_t ty = t / (uint32_t)C.tiles_x, tx = t - ty * (uint32_t)C.tiles_x;
+    const uint32_t ly = pix / (uint32_t)C.tile_w;
+    px = (int)(tx * (uint32_t)C.tile_w + (pix - ly * (uint32_t)C.tile_w));
+    py = (int)(ty * (uint32_t)C.tile_h + ly);
+    return px < C.W && py < C.H;
+}
+
+template <typename S>
+__global__ void k_compose(const ComposeParams C) {
+    const uint32_t tile_px = (uint32_t)(C.tile_w * C.tile_h);
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)C.n_local_tiles * tile_px) return;
+    const uint32_t lt = (uint32_t)(i / tile_px), pix = (uint32_t)(i - (size_t)lt * tile_px);
+    int px, py;
+    if (!tile_pixel(C, lt, pix, px, py)) return;
+    const S *s = reinterpret_cast<const S *>(C.slots) + 3 * i * (size_t)C.spp;
+    S acc0 = 0, acc1 = 0, acc2 = 0;
+    for (int k = 0; k < C.spp; ++k) {
+        acc0 += s[3 * k];
+        acc1 += s[3 * k + 1];
+        acc2 += s[3 * k + 2];
+    }
+    float *o = C.out + 3 * ((size_t)py * C.W + px);
+    o[0] = (float)(acc0 / (S)C.spp);
+    o[1] = (float)(acc1 / (S)C.spp);
+    o[2] = (float)(acc2 / (S)C.spp);
+}
+
+__global__ void k_tiles_pack(const ComposeParams C, const float *frame, float *packed) {
+    const uint32_t tile_px = (uint32_t)(C.tile_w * C.tile_h);
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)C.n_local_tiles * tile_px) return;
+    const uint32_t lt = (uint32_t)(i / tile_px), pix = (uint32_t)(i - (size_t)lt * tile_px);
+    int px, py;
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+    if (tile_pixel(C, lt, pix, px, py)) {
+        const float *f = frame + 3 * ((size_t)py * C.W + px);
+        v0 = f[0];
+        v1 = f[1];
+        v2 = f[2];
+    }
+    packed[3 * i] = v0;
+    packed[3 * i + 1] = v1;
+    packed[3 * i + 2] = v2;
+}
+
+// packed_all = shard_count consecutive buffers of per_shard floats; shard r's
+// local tile j is global tile j*shard_count + r.
+__global__ void k_tiles_unpack(ComposeParams C, const float *packed_all, size_t per_shard,
+                               float *frame) {
+    const uint32_t tile_px = (uint32_t)(C.tile_w * C.tile_h);
+    const uint32_t tiles_y = (uint32_t)((C.H + C.tile_h - 1) / C.tile_h);
+    const size_t n_tiles = (size_t)C.tiles_x * tiles_y;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_tiles * tile_px) return;
+    const uint32_t t = (uint32_t)(i / tile_px), pix = (uint32_t)(i - (size_t)t * tile_px);
+    const uint32_t r = t % (uint32_t)C.shard_count, lt = t / (uint32_t)C.shard_count;
+    C.shard_index = (int)r;
+    int px, py;
+    if (!tile_pixel(C, lt, pix, px, py)) return;
+    const float *src = packed_all + r * per_shard + 3 * ((size_t)lt * tile_px + pix);
+    float *dst = frame + 3 * ((size_t)py * C.W + px);
+    dst[0] = src[0];
+    dst[1] = src[1];
+    dst[2] = src[2];
+}
+
+cudaError_t launch_compose(bool parity, const ComposeParams &C, cudaStream_t st) {
+    const size_t n = (size_t)C.n_local_tiles * C.tile_w * C.tile_h;
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (parity) k_compose<double><<<blocks, 256, 0, st>>>(C);
+    else k_compose<float><<<blocks, 256, 0, st>>>(C);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tiles_pack(const ComposeParams &C, const float *frame, float *packed,
+                              cudaStream_t st) {
+    const size_t n = (size_t)C.n_local_tiles * C.tile_w * C.tile_h;
+    if (n == 0) return cudaSuccess;
+    k_tiles_pack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(C, frame, packed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tiles_unpack(const ComposeParams &C, const float *packed_all,
+                                size_t per_shard_floats, float *frame, cudaStream_t st) {
+    const size_t tiles_y = (size_t)((C.H + C.tile_h - 1) / C.tile_h);
+    const size_t n = (size_t)C.tiles_x * tiles_y * C.tile_w * C.tile_h;
+    if (n == 0) return cudaSuccess;
+    k_tiles_unpack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(C, packed_all, per_shard_floats,
+                                                                 frame);
+    return cudaGetLastError();
+}
+
+}  // namespace pfk

@@ -1,0 +1,369 @@
+// pf_knn.cu -- K6/K7: phase-selective exact KNN + fused Eq. 6 / Eq. 7.
+//
+// SPEC.md:221-280 (photon_map: build / knn_phase), SPEC.md:282-316 (Eq. 6
+// estimate_radiance, Eq. 7 encode_log), SPEC.md:476-484 (make_batch).
+//
+// B200 design.  The reference's "single kd-tree with phase filtering" is a
+// pointer-chasing structure; on the GPU the photon map becomes a per-phase
+// uniform cell grid built by a radix sort on (phase, cell) keys, so every
+// cell's photons of ONE phase are contiguous 16-byte records {x,y,z,id}.
+// A query is one warp: lanes stream candidate records of a cell in
+// coalesced 512-byte rows, and the warp keeps the exact top-K as a sorted,
+// lane-distributed list of 64-bit keys (float_bits(d2) << 32 | id) -- the
+// (d2, id) lexicographic order the oracle uses, so ties break by photon id.
+// Cells are visited in Chebyshev rings around the query cell and skipped
+// when their (conservatively expanded) box distance cannot beat the current
+// K-th key; the search stops when the ring bound exceeds the K-th distance
+// or r_max.  The result is therefore exactly the brute-force answer.
+//
+// Compiled with --fmad=false: d2 = ((dx*dx)+(dy*dy))+(dz*dz) in binary32 and
+// Eq. 6 in binary64 must round exactly like the oracle.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "pf_knn.h"
+
+namespace pfk {
+
+// ---- build ---------------------------------------------------------------
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void k_knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins,
+                           uint32_t *maxs, uint32_t *counts) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const PhotonRec p = ph[i];
+    const int g = p.g_index;
+    if (g >= n_phases) return;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        atomicMin(&mins[3 * g + a], f2ord(p.position[a]));
+        atomicMax(&maxs[3 * g + a], f2ord(p.position[a]));
+    }
+    atomicAdd(&counts[g], 1u);
+}
+
+__device__ __forceinline__ int cell_axis(double p, double lo, double inv_h, int R) {
+    double c = floor((p - lo) * inv_h);
+    int ci = c < 0.0 ? 0 : (c > (double)(R - 1) ? R - 1 : (int)c);
+    return ci;
+}
+
+__global__ void k_knn_keys(const PhotonRec *ph, size_t n, const KnnParams P, uint32_t *keys,
+                           uint32_t *vals, uint32_t *hist) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const PhotonRec p = ph[i];
+    uint32_t key = P.total_cells;  // photons of unknown phases sort past the end
+    if (p.g_index < P.n_phases) {
+        const KnnGrid &G = P.grid[p.g_index];
+        const int cx = cell_axis(p.position[0], G.lo[0], G.inv_h[0], G.R[0]);
+        const int cy = cell_axis(p.position[1], G.lo[1], G.inv_h[1], G.R[1]);
+        const int cz = cell_axis(p.position[2], G.lo[2], G.inv_h[2], G.R[2]);
+        key = G.cell_base + (uint32_t)cx + (uint32_t)G.R[0] * ((uint32_t)cy + (uint32_t)G.R[1] * (uint32_t)cz);
+        atomicAdd(&hist[key], 1u);
+    }
+    keys[i] = key;
+    vals[i] = (uint32_t)i;
+}
+
+__global__ void k_knn_gather(const PhotonRec *ph, size_t n, const uint32_t *vals, float4 *spos) {
+    const size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint32_t id = vals[j];
+    const PhotonRec p = ph[id];
+    spos[j] = make_float4(p.position[0], p.position[1], p.position[2], __uint_as_float(id));
+}
+
+// ---- query ---------------------------------------------------------------
+template <int KP>
+struct WarpTopK {
+    uint64_t v[KP];  // list position p = s*32 + lane, ascending
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int s = 0; s < KP; ++s) v[s] = ~0ull;
+    }
+    __device__ __forceinline__ uint64_t at(int p) const {
+        uint64_t r = 0;
+#pragma unroll
+        for (int s = 0; s < KP; ++s)
+            if (s == (p >> 5)) r = v[s];
+        return __shfl_sync(0xffffffffu, r, p & 31);
+    }
+    __device__ __forceinline__ void insert(uint64_t key, unsigned lane) {
+        int pos = 0;
+#pragma unroll
+        for (int s = 0; s < KP; ++s) pos += __popc(__ballot_sync(0xffffffffu, v[s] < key));
+        uint64_t carry = 0;
+#pragma unroll
+        for (int s = 0; s < KP; ++s) {
+            const uint64_t up = __shfl_up_sync(0xffffffffu, v[s], 1);
+            const uint64_t last = __shfl_sync(0xffffffffu, v[s], 31);
+            const uint64_t nv = lane == 0 ? carry : up;
+            carry = last;
+            const int p = s * 32 + (int)lane;
+            v[s] = p > pos ? nv : (p == pos ? key : v[s]);
+        }
+    }
+};
+
+__device__ __forceinline__ float d2_rn(float4 c, const float q[3]) {
+    const float dx = __fsub_rn(c.x, q[0]), dy = __fsub_rn(c.y, q[1]), dz = __fsub_rn(c.z, q[2]);
+    return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+}
+
+// hg_eval (phase.hpp:18-23), binary64, no contraction (TU built --fmad=false).
+__device__ __forceinline__ double knn_hg_eval(double g, double c) {
+    g = g < -0.999 ? -0.999 : (g > 0.999 ? 0.999 : g);
+    double denom = 1.0 + g * g - 2.0 * g * c;
+    denom = denom < 1e-12 ? 1e-12 : denom;
+    return (1.0 / (4.0 * 3.14159265358979323846)) * (1.0 - g * g) / (denom * sqrt(denom));
+}
+
+template <int KP>
+__global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
+    const unsigned lane = threadIdx.x & 31u;
+    const size_t qi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (qi >= P.nq) return;
+    const int K = P.K;
+    const float q[3] = {P.qx[3 * qi], P.qx[3 * qi + 1], P.qx[3 * qi + 2]};
+    const int g = P.qg[qi];
+    WarpTopK<KP> top;
+    top.init();
+    int count = 0;
+    uint64_t thr = ~0ull;  // key of the K-th entry (inf while count < K)
+    const float r2 = P.r2;
+
+    if (g < P.n_phases && P.grid[g].n > 0) {
+        const KnnGrid &G = P.grid[g];
+        int qc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) qc[a] = cell_axis((double)q[a], G.lo[a], G.inv_h[a], G.R[a]);
+        const int rmax = max(G.R[0], max(G.R[1], G.R[2]));
+        for (int ring = 0; ring <= rmax; ++ring) {
+            for (int dz = -ring; dz <= ring; ++dz) {
+                const int cz = qc[2] + dz;
+                if (cz < 0 || cz >= G.R[2]) continue;
+                for (int dy = -ring; dy <= ring; ++dy) {
+                    const int cy = qc[1] + dy;
+                    if (cy < 0 || cy >= G.R[1]) continue;
+                    const bool yz_shell = abs(dz) == ring || abs(dy) == ring;
+                    for (int dx = -ring; dx <= ring; dx += (yz_shell ? 1 : 2 * max(ring, 1))) {
+                        const int cx = qc[0] + dx;
+                        if (cx < 0 || cx >= G.R[0]) continue;
+                        const int c3[3] = {cx, cy, cz};
+                        // conservative box distance (expanded by eps_abs; edge cells unbounded)
+                        double lb = 0.0;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const double lo = c3[a] == 0 ? -1e300 : G.lo[a] + c3[a] * G.h[a] - G.eps;
+                            const double hi = c3[a] == G.R[a] - 1 ? 1e300
+                                                                  : G.lo[a] + (c3[a] + 1) * G.h[a] + G.eps;
+                            const double dq = (double)q[a];
+                            const double d = dq < lo ? lo - dq : (dq > hi ? dq - hi : 0.0);
+                            lb += d * d;
+                        }
+                        lb *= (1.0 - 1e-5);
+                        if (lb > (double)r2) continue;
+                        if (count >= K && lb > (double)__uint_as_float((uint32_t)(thr >> 32))) continue;
+                        const uint32_t cell =
+                            G.cell_base + (uint32_t)cx + (uint32_t)G.R[0] * ((uint32_t)cy + (uint32_t)G.R[1] * (uint32_t)cz);
+                        const uint32_t b = P.cell_start[cell], e = P.cell_start[cell + 1];
+                        for (uint32_t j0 = b; j0 < e; j0 += 32) {
+                            const uint32_t j = j0 + lane;
+                            uint64_t key = ~0ull;
+                            if (j < e) {
+                                const float4 c = __ldg(&P.spos[j]);
+                                const float d2 = d2_rn(c, q);
+                                if (d2 <= r2) key = ((uint64_t)__float_as_uint(d2) << 32) | __float_as_uint(c.w);
+                            }
+                            unsigned m = __ballot_sync(0xffffffffu, key < thr);
+                            while (m) {
+                                const int src = __ffs(m) - 1;
+                                const uint64_t k = __shfl_sync(0xffffffffu, key, src);
+                                top.insert(k, lane);
+                                if (count < K) ++count;
+                                if (count >= K) thr = top.at(K - 1);
+                                m &= ~(1u << src);
+                                m &= __ballot_sync(0xffffffffu, key < thr);
+                            }
+                        }
+                    }
+                }
+            }
+            // all cells at Chebyshev distance > ring are >= ring*h_min - 2eps away
+            const double bnd = fmax(0.0, ring * G.hmin - 2.0 * G.eps);
+            const double bnd2 = bnd * bnd * (1.0 - 1e-5);
+            if (bnd2 > (double)r2) break;
+            if (count >= K && bnd2 > (double)__uint_as_float((uint32_t)(thr >> 32))) break;
+        }
+    }
+
+    // ---- outputs: ids / d2 / counts
+    if (P.out_ids || P.out_d2) {
+#pragma unroll
+        for (int s = 0; s < KP; ++s) {
+            const int p = s * 32 + (int)lane;
+            if (p < K) {
+                const bool live = p < count;
+                if (P.out_ids) P.out_ids[qi * K + p] = live ? (uint32_t)top.v[s] : 0xFFFFFFFFu;
+                if (P.out_d2)
+                    P.out_d2[qi * K + p] =
+                        live ? __uint_as_float((uint32_t)(top.v[s] >> 32)) : __int_as_float(0x7f800000);
+            }
+        }
+    }
+    if (P.out_counts && lane == 0) P.out_counts[qi] = count;
+    if (!P.out_targets) return;
+
+    // ---- fused Eq. 6 (binary64, sequential in list order) + Eq. 7
+    double L[3] = {0.0, 0.0, 0.0};
+    if (count > 0) {
+        const double r = sqrt((double)__uint_as_float((uint32_t)(top.at(count - 1) >> 32)));
+        if (!(r < 1e-6)) {
+            const double w[3] = {P.qw[3 * qi], P.qw[3 * qi + 1], P.qw[3 * qi + 2]};
+            const double gv = P.phase[g];
+            double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < KP; ++s) {
+                if (s * 32 >= count) break;
+                const int p = s * 32 + (int)lane;
+                double term[3] = {0.0, 0.0, 0.0};
+                if (p < count) {
+                    const PhotonRec ph = P.photons[(uint32_t)top.v[s]];
+                    const double c = w[0] * (double)ph.direction[0] + w[1] * (double)ph.direction[1] +
+                                     w[2] * (double)ph.direction[2];
+                    const double f = knn_hg_eval(gv, c);
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) term[ch] = f * (double)ph.power[ch];
+                }
+                // sequential sum in list order (bit-identical to the oracle loop)
+                const int n_here = min(32, count - s * 32);
+                for (int k = 0; k < n_here; ++k) {
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) acc[ch] += __shfl_sync(0xffffffffu, term[ch], k);
+                }
+            }
+            const double vol = (4.0 / 3.0) * 3.14159265358979323846 * (r * r * r);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) L[ch] = acc[ch] / vol;
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const double v = L[ch];
+            double t;
+            if (v > 1.0) t = 0.0;
+            else if (v > P.enc_threshold) t = -log10(v) / P.psi;
+            else t = 1.0;
+            P.out_targets[3 * qi + ch] = t;
+        }
+    }
+}
+
+// make_batch query generation (oracle or_make_queries).
+__device__ __forceinline__ uint32_t mq_u32(uint64_t &st, uint64_t inc) {
+    uint64_t old = st;
+    st = old * 6364136223846793005ULL + inc;
+    uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
+    uint32_t rot = (uint32_t)(old >> 59);
+    return __funnelshift_r(xs, xs, rot);
+}
+__device__ __forceinline__ double mq_double(uint64_t &st, uint64_t inc) {
+    uint64_t hi = mq_u32(st, inc);
+    uint64_t lo = mq_u32(st, inc);
+    return (double)(((hi << 32) | lo) >> 11) * 0x1.0p-53;
+}
+
+__global__ void k_make_queries(uint64_t initstate, uint64_t base, size_t batch, int n_phases,
+                               float *x3, double *w3, uint8_t *gidx) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch) return;
+    const uint64_t inc = ((base + i) << 1) | 1ull;
+    uint64_t st = 0;
+    mq_u32(st, inc);
+    st += initstate;
+    mq_u32(st, inc);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x3[3 * i + a] = (float)mq_double(st, inc);
+    const double z = 1.0 - 2.0 * mq_double(st, inc);
+    const double phi = (2.0 * 3.14159265358979323846) * mq_double(st, inc);
+    const double t = 1.0 - z * z;
+    const double rr = sqrt(t > 0.0 ? t : 0.0);
+    w3[3 * i] = rr * cos(phi);
+    w3[3 * i + 1] = rr * sin(phi);
+    w3[3 * i + 2] = z;
+    gidx[i] = (uint8_t)(((uint64_t)mq_u32(st, inc) * (uint64_t)n_phases) >> 32);
+}
+
+// ---- host --------------------------------------------------------------
+cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins, uint32_t *maxs,
+                     uint32_t *counts, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_knn_bbox<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ph, n, n_phases, mins, maxs, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffers &B,
+                     cudaStream_t st) {
+    cudaError_t e;
+    const size_t ncells = (size_t)P.total_cells + 1;
+    if ((e = B.keys.ensure(n * 4)) || (e = B.vals.ensure(n * 4)) || (e = B.keys2.ensure(n * 4)) ||
+        (e = B.vals2.ensure(n * 4)) || (e = B.hist.ensure(ncells * 4)) ||
+        (e = B.cell_start.ensure((ncells + 1) * 4)) || (e = B.spos.ensure(n * 16)))
+        return e;
+    cudaMemsetAsync(B.hist.p, 0, ncells * 4, st);
+    if (n) {
+        k_knn_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ph, n, P, (uint32_t *)B.keys.p,
+                                                                (uint32_t *)B.vals.p, (uint32_t *)B.hist.p);
+        if ((e = cudaGetLastError())) return e;
+    }
+    // stable radix sort by cell key keeps ids ascending inside a cell
+    int end_bit = 1;
+    while (end_bit < 32 && (1ull << end_bit) <= (uint64_t)P.total_cells) ++end_bit;
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, (uint32_t *)B.keys.p, (uint32_t *)B.keys2.p,
+                                    (uint32_t *)B.vals.p, (uint32_t *)B.vals2.p, (int)n, 0, end_bit, st);
+    if ((e = B.temp.ensure(tmp + 256))) return e;
+    cub::DeviceRadixSort::SortPairs(B.temp.p, tmp, (uint32_t *)B.keys.p, (uint32_t *)B.keys2.p,
+                                    (uint32_t *)B.vals.p, (uint32_t *)B.vals2.p, (int)n, 0, end_bit, st);
+    size_t tmp2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (uint32_t *)B.hist.p, (uint32_t *)B.cell_start.p,
+                                  (int)ncells, st);
+    if ((e = B.temp2.ensure(tmp2 + 256))) return e;
+    cub::DeviceScan::ExclusiveSum(B.temp2.p, tmp2, (uint32_t *)B.hist.p, (uint32_t *)B.cell_start.p,
+                                  (int)ncells, st);
+    if (n) {
+        k_knn_gather<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ph, n, (const uint32_t *)B.vals2.p,
+                                                                  (float4 *)B.spos.p);
+        if ((e = cudaGetLastError())) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {
+    if (P.nq == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((P.nq * 32 + 127) / 128);
+    const int kp = (P.K + 31) / 32;
+    if (kp <= 1) k_knn_query<1><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 2) k_knn_query<2><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 4) k_knn_query<4><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 8) k_knn_query<8><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 16) k_knn_query<16><<<blocks, 128, 0, st>>>(P);
+    else k_knn_query<32><<<blocks, 128, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t knn_make_queries(uint64_t initstate, uint64_t base, size_t batch, int n_phases,
+                             float *x3, double *w3, uint8_t *gidx, cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    k_make_queries<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(initstate, base, batch, n_phases,
+                                                                     x3, w3, gidx);
+    return cudaGetLastError();
+}
+
+}  // namespace pfk

@@ -1,0 +1,63 @@
+// pf_knn.h -- photon map (per-phase cell grid) + KNN internals.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pf_kernels.h"
+
+#define PF_MAX_PHASES 8
+
+namespace pfk {
+
+struct PhotonRec {  // == pf_photon (photon.hpp:17-22), 40 bytes
+    float position[3];
+    float direction[3];
+    float power[3];
+    uint8_t g_index;
+    uint8_t pad_[3];
+};
+static_assert(sizeof(PhotonRec) == 40, "PhotonRec must be 40 B");
+
+struct KnnGrid {
+    double lo[3], h[3], inv_h[3];
+    double hmin, eps;  // smallest cell edge; absolute bound slack
+    int R[3];
+    uint32_t cell_base;
+    uint32_t n;        // photons of this phase
+};
+
+struct KnnParams {
+    int n_phases;
+    uint32_t total_cells;
+    KnnGrid grid[PF_MAX_PHASES];
+    double phase[PF_MAX_PHASES];
+    const float4 *spos;           // sorted {x, y, z, id}
+    const uint32_t *cell_start;   // total_cells + 1
+    const PhotonRec *photons;     // load order (ids)
+    size_t nq;
+    const float *qx;
+    const uint8_t *qg;
+    const double *qw;
+    int K;
+    float r2;
+    double psi, enc_threshold;    // Eq. 7: 10^-psi
+    uint32_t *out_ids;
+    float *out_d2;
+    int32_t *out_counts;
+    double *out_targets;
+};
+
+struct KnnBuffers {
+    DevBuf keys, vals, keys2, vals2, hist, cell_start, spos, temp, temp2;
+};
+
+cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins, uint32_t *maxs,
+                     uint32_t *counts, cudaStream_t st);
+cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffers &B,
+                     cudaStream_t st);
+cudaError_t knn_query(const KnnParams &P, cudaStream_t st);
+cudaError_t knn_make_queries(uint64_t initstate, uint64_t base, size_t batch, int n_phases,
+                             float *x3, double *w3, uint8_t *gidx, cudaStream_t st);
+
+}  // namespace pfk

@@ -1,0 +1,110 @@
+"""KNN training-target gather (config 3) on the GPU vs the oracle.
+
+Photon ids (and their order) must be BIT-EXACT (north_star).  d2 values are
+the binary32 ((dx*dx)+(dy*dy))+(dz*dz) and must match bitwise too.  Targets
+(Eq. 6 binary64 + Eq. 7 log10) may differ only by libm last-bit rounding:
+|dt| <= 1e-14.
+"""
+import numpy as np
+import pytest
+
+from paper_2304_07338_b200.scene import make_photons, synth_photons
+
+pytestmark = pytest.mark.gpu
+PHASES = [-0.75, 0.0, 0.75]
+
+
+def _check_against_brute(ctx, oracle, ph, q, g, K, r):
+    ids, d2, cnt = ctx.knn_query(q, g, K, r)
+    for i in range(len(q)):
+        ri, rd = oracle.knn_brute(ph, q[i], int(g[i]), K, r)
+        assert cnt[i] == len(ri), (i, K, r)
+        assert np.array_equal(ids[i, : cnt[i]], ri), (i, K, r)
+        assert np.array_equal(d2[i, : cnt[i]].view(np.uint32), rd.view(np.uint32))
+        assert np.all(ids[i, cnt[i]:] == 0xFFFFFFFF)
+
+
+@pytest.mark.parametrize("K", [1, 8, 1024])
+@pytest.mark.parametrize("r", [0.05, 0.5, float("inf")])
+def test_knn_equals_brute_force(ctx, oracle, K, r):
+    """1e4 photons x 1e3 queries, same ids, same order."""
+    ph = synth_photons(10000, 3, seed=1)
+    ctx.knn_build(ph, PHASES)
+    rq = np.random.default_rng(2)
+    q = rq.random((1000, 3)).astype(np.float32)
+    g = rq.integers(0, 3, 1000).astype(np.uint8)
+    _check_against_brute(ctx, oracle, ph, q, g, K, r)
+
+
+def test_knn_ties_and_clusters(ctx, oracle):
+    ph = synth_photons(20000, 3, seed=3, clustered=True)
+    # exact duplicates -> ties broken by id
+    ph["position"][5000:5400] = ph["position"][5000]
+    ph["g_index"][5000:5400] = 1
+    ctx.knn_build(ph, PHASES)
+    q = np.concatenate([ph["position"][5000:5010], np.random.default_rng(4).random((300, 3))]
+                       ).astype(np.float32)
+    q[-5:] = [[-0.5, 0.5, 0.5], [1.5, 1.5, 1.5], [0.5, -2, 0.5], [0, 0, 0], [1, 1, 1]]
+    g = np.ones(len(q), np.uint8)
+    for K in (64, 500):
+        _check_against_brute(ctx, oracle, ph, q, g, K, float("inf"))
+        _check_against_brute(ctx, oracle, ph, q, g, K, 0.02)
+
+
+def test_knn_empty_and_single(ctx, oracle):
+    one = make_photons(np.array([[0.5, 0.5, 0.5]], np.float32), np.array([[0, 0, 1]], np.float32),
+                       np.ones((1, 3), np.float32), np.array([2]))
+    ctx.knn_build(one, PHASES)
+    ids, d2, cnt = ctx.knn_query(np.array([[0.5, 0.5, 0.5], [0.1, 0.1, 0.1]], np.float32),
+                                 np.array([2, 0], np.uint8), 4)
+    assert list(cnt) == [1, 0] and ids[0, 0] == 0 and d2[0, 0] == 0.0
+    tg = ctx.knn_targets(np.array([[0.1, 0.1, 0.1]], np.float32), np.array([[0, 0, 1.0]]),
+                         np.array([0], np.uint8), 8)
+    assert np.all(tg == 1.0)                         # empty -> encode_log(0) = 1
+
+
+def test_knn_targets_match_oracle(ctx, oracle):
+    ph = synth_photons(50000, 3, seed=7)
+    ph["power"] *= 2e-3
+    ctx.knn_build(ph, PHASES)
+    x, w, g = oracle.make_queries(11, 0, 2000, 3)
+    kd = oracle.KdTree(ph)
+    for K, r in [(64, float("inf")), (64, 0.05), (16, 0.25)]:
+        tg, ids, d2, cnt = ctx.knn_targets(x, w, g, K, r, 5.0, with_ids=True)
+        rtg, rids, rd2, rcnt = kd.targets(x, w, g, PHASES, K, r, 5.0)
+        assert np.array_equal(cnt, rcnt)
+        for i in range(len(x)):
+            assert np.array_equal(ids[i, : cnt[i]], rids[i, : cnt[i]])
+        assert np.all((tg >= 0) & (tg <= 1))
+        assert np.max(np.abs(tg - rtg)) <= 1e-14
+
+
+def test_make_batch_matches_oracle(ctx, oracle):
+    ph = synth_photons(30000, 3, seed=8)
+    ph["power"] *= 1e-3
+    ctx.knn_build(ph, PHASES)
+    x, w, g, t = ctx.make_batch(seed=5, step=3, batch=4096, K=32, r_max=0.5)
+    ox, ow, og = oracle.make_queries(5, 3, 4096, 3)
+    assert np.array_equal(x, ox) and np.array_equal(g, og)
+    assert np.max(np.abs(w - ow)) < 1e-15
+    otg, _, _, _ = oracle.KdTree(ph).targets(ox, ow, og, PHASES, 32, 0.5, 5.0)
+    assert np.max(np.abs(t - otg)) <= 1e-12
+    # g marginal uniform over G (chi-square alpha = 0.01)
+    from scipy import stats
+    assert stats.chisquare(np.bincount(g, minlength=3)).pvalue > 0.01
+
+
+def test_knn_full_size_sampled(ctx, oracle):
+    """Config 3 size: 4M photons, K = 64 -- exact on a random query sample."""
+    ph = synth_photons(4_000_000, 3, seed=9)
+    ctx.knn_build(ph, PHASES)
+    rq = np.random.default_rng(10)
+    q = rq.random((20000, 3)).astype(np.float32)
+    g = rq.integers(0, 3, 20000).astype(np.uint8)
+    ids, d2, cnt = ctx.knn_query(q, g, 64, float("inf"))
+    assert np.all(cnt == 64)
+    assert np.all(np.diff(d2, axis=1) >= 0)
+    kd = oracle.KdTree(ph)
+    for i in rq.choice(20000, 300, replace=False):
+        ri, rd = kd.knn(q[i], int(g[i]), 64)
+        assert np.array_equal(ids[i], ri)

@@ -1,0 +1,134 @@
+"""End-to-end render_neural on the GPU vs the oracle (config 1 and variants).
+
+Tolerances:
+  * PARITY mode, L_i off: binary64 tracking + delta-trial NEE must reproduce
+    the oracle frame; pixels may differ only where CUDA's log() rounds a last
+    bit differently from glibc -> <= 1e-3 of pixels differ, none by > 1e-5 rel.
+  * PARITY mode, L_i on: the field runs in fp16/fp32 (test_gpu_field), so the
+    frame must agree to per-pixel RMSE <= 2e-3 * mean radiance + 1e-6.
+  * FAST mode (binary32 + ratio tracking): statistical -- a 64-spp frame
+    agrees with the 64-spp parity frame to relative RMSE <= 5%.
+  * Shard/tiling invariance is exact (byte-identical) in both modes.
+"""
+import numpy as np
+import pytest
+
+from paper_2304_07338_b200 import FieldConfig, RenderConfig
+from paper_2304_07338_b200.scene import CameraSpec, default_lights, synth_volume, tf_scene_a, tf_scene_b
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def config1(ctx, oracle):
+    """BASELINE config 1: 64^3 synthetic volume, 256x256, 1 spp, small field, one light."""
+    vol = synth_volume("sphere_sinusoid", 64)
+    tf = tf_scene_b()
+    ctx.upload_volume(vol)
+    ctx.set_medium(tf, 100.0)
+    ctx.set_lights(default_lights())
+    fc = FieldConfig.desk()
+    params = fc.init_params(seed=4, embed_scale=0.5, bias_scale=0.1)
+    ctx.load_field(fc, params)
+    return ctx, oracle.OracleScene(vol, tf, 100.0), fc, params
+
+
+def test_parity_direct_light_matches_oracle(config1, oracle):
+    ctx, osc, fc, params = config1
+    cam = CameraSpec(256, 256)
+    rc = RenderConfig(spp=1, g=0.25, seed=42, mode="parity", use_field=False,
+                      background=(0.05, 0.1, 0.2))
+    img, st = ctx.render_neural(cam, rc, stats=True)
+    ref, ost = oracle.render_neural(osc, default_lights(), None, None, cam, rc)
+    assert st["samples"] == ost["samples"] == 256 * 256
+    assert abs(st["hits"] - ost["hits"]) <= 2
+    diff = img != ref
+    n_diff = np.count_nonzero(np.any(diff, axis=2))
+    print("pixels differing:", n_diff, "hits", st["hits"])
+    assert n_diff <= 1e-3 * 256 * 256
+    assert np.allclose(img, ref, rtol=1e-5, atol=1e-7) or n_diff <= 3
+
+
+def test_parity_with_field_matches_oracle(config1, oracle):
+    ctx, osc, fc, params = config1
+    cam = CameraSpec(128, 96)
+    rc = RenderConfig(spp=2, g=0.0, seed=7, mode="parity", use_field=True, w_d=1.0, w_i=1.0)
+    img = ctx.render_neural(cam, rc)
+    ref, _ = oracle.render_neural(osc, default_lights(), fc, params, cam, rc)
+    rmse = np.sqrt(np.mean((img.astype(np.float64) - ref) ** 2))
+    print("rmse", rmse, "mean", ref.mean())
+    assert rmse <= 2e-3 * ref.mean() + 1e-6
+
+
+def test_fast_mode_statistically_equal(config1):
+    ctx, _, _, _ = config1
+    cam = CameraSpec(64, 64)
+    par = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=1, mode="parity"))
+    fast = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=1, mode="fast"))
+    rel = np.sqrt(np.mean((fast - par) ** 2)) / par.mean()
+    print("fast vs parity rel rmse", rel)
+    assert rel < 0.05
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_shard_and_tile_invariance(config1, mode):
+    import torch
+    ctx, _, _, _ = config1
+    cam = CameraSpec(200, 120)
+    base = RenderConfig(spp=3, g=-0.3, seed=9, mode=mode, tile=(16, 16))
+    ref = ctx.render_neural(cam, base)
+    for tile, shards in [((8, 8), 1), ((16, 16), 3), ((32, 8), 8)]:
+        frame = torch.zeros((120, 200, 3), dtype=torch.float32, device="cuda")
+        for s in range(shards):
+            rc = RenderConfig(spp=3, g=-0.3, seed=9, mode=mode, tile=tile, shard_index=s,
+                              shard_count=shards)
+            ctx.render_neural(cam, rc, out=frame)
+        ctx.synchronize()
+        assert np.array_equal(frame.cpu().numpy().view(np.uint32), ref.view(np.uint32)), (tile, shards)
+
+
+def test_tiles_pack_unpack_roundtrip(config1):
+    import torch
+    ctx, _, _, _ = config1
+    spec = CameraSpec(100, 70)
+    cam = ctx.camera(spec)
+    ref = ctx.render_neural(spec, RenderConfig(spp=1, seed=2))
+    shards = 3
+    per = max(ctx.tiles_count(cam, RenderConfig(shard_count=shards, shard_index=s), s)
+              for s in range(shards)) * 16 * 16 * 3
+    packed = torch.zeros(shards * per, dtype=torch.float32, device="cuda")
+    for s in range(shards):
+        rc = RenderConfig(spp=1, seed=2, shard_index=s, shard_count=shards)
+        frame = torch.zeros((70, 100, 3), dtype=torch.float32, device="cuda")
+        ctx.render_neural(cam, rc, out=frame)
+        ctx.tiles_pack(cam, rc, frame, packed[s * per:(s + 1) * per])
+    out = torch.zeros((70, 100, 3), dtype=torch.float32, device="cuda")
+    ctx.tiles_unpack(cam, RenderConfig(spp=1, seed=2, shard_count=shards), packed, per, out)
+    ctx.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_vacuum_renders_background(ctx):
+    """alpha == 0 -> every pixel equals the background exactly."""
+    ctx.upload_volume(synth_volume("sphere_sinusoid", 16))
+    ctx.set_medium(np.array([[0, 1, 1, 1, 0], [1, 1, 1, 1, 0]], np.float64), 100.0)
+    ctx.set_lights(default_lights())
+    for mode in ("parity", "fast"):
+        img = ctx.render_neural(CameraSpec(32, 32), RenderConfig(spp=2, mode=mode, use_field=False,
+                                                                 background=(0.3, 0.2, 0.1)))
+        assert np.all(img == np.array([0.3, 0.2, 0.1], np.float32))
+
+
+def test_render_validation(ctx):
+    ctx.upload_volume(synth_volume("sphere", 16))
+    ctx.set_medium(tf_scene_a(), 100.0)
+    ctx.set_lights(default_lights())
+    with pytest.raises(ValueError):
+        ctx.render_neural(CameraSpec(8, 8), RenderConfig(spp=0, use_field=False))
+    ctx.set_lights(np.zeros((0, 6)))
+    with pytest.raises(ValueError):
+        ctx.render_neural(CameraSpec(8, 8), RenderConfig(spp=1, use_field=False))
+    with pytest.raises(ValueError):
+        ctx.set_medium(np.array([[0.1, 1, 1, 1, 0], [1, 1, 1, 1, 1]]), 100.0)
+    with pytest.raises(ValueError):
+        ctx.upload_volume(np.full((4, 4, 4), 1.5, np.float32))

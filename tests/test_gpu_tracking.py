@@ -1,0 +1,133 @@
+"""GPU parts (a)/(b) through the C ABI vs the oracle: RNG, delta_track, transmittance.
+
+Tolerances (stated per north_star): RNG streams, hit/miss decisions and
+transmittance trial outcomes are integer-valued -> compared exactly.  Binary64
+interaction positions are compared bit-for-bit; the only permitted source of
+difference is CUDA's log() vs glibc's log() rounding a last bit differently,
+so we allow at most 1e-4 of hits to differ, and those by <= 1e-12.
+"""
+import numpy as np
+import pytest
+
+from paper_2304_07338_b200.scene import synth_volume, tf_scene_a, tf_scene_b
+
+pytestmark = pytest.mark.gpu
+CAM, NEE, TEST = 3, 4, 8
+
+
+def _rays(n, seed=0):
+    r = np.random.default_rng(seed)
+    o = r.uniform(-0.5, 1.5, (n, 3))
+    o[: n // 4] = r.uniform(0, 1, (n // 4, 3))
+    d = r.standard_normal((n, 3))
+    d[n // 4: n // 4 + 64, 0] = 0.0
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o[n // 4 + 128: n // 4 + 160] = [0.0, 0.5, -1.0]
+    d[n // 4 + 128: n // 4 + 160] = [0.0, 0.0, 1.0]
+    tmin = np.zeros(n)
+    tmin[::7] = r.uniform(0, 0.5, len(tmin[::7]))
+    tmax = np.full(n, np.inf)
+    tmax[::5] = r.uniform(0.6, 3.0, len(tmax[::5]))
+    return o, d, tmin, tmax
+
+
+@pytest.fixture(scope="module", params=["a", "b"])
+def scene(request, ctx, oracle):
+    tf = tf_scene_a() if request.param == "a" else tf_scene_b()
+    vol = synth_volume("sphere_sinusoid", 64)
+    ctx.upload_volume(vol)
+    ctx.set_medium(tf, 100.0)
+    ctx.set_lights([[2.0, 2.5, -1.0, 1.0, 1.0, 1.0]])
+    osc = oracle.OracleScene(vol, tf, 100.0)
+    return ctx, osc
+
+
+def test_device_rng_bitwise(ctx, oracle):
+    import ctypes as C
+    idx = (np.arange(100000, dtype=np.uint64) * 7919) ^ np.uint64(0xABCDEF)
+    dev = ctx.rng_doubles(1234, "camera", idx, 8)
+    ref = np.zeros((len(idx), 8))
+    oracle.lib().or_rng_doubles(1234, CAM, len(idx), idx.ctypes.data, 8, ref.ctypes.data)
+    assert np.array_equal(dev.view(np.uint64), ref.view(np.uint64))
+    # SURVEY App. A golden: make_rng(7, CameraSample, 12345)
+    v = ctx.rng_doubles(7, "camera", np.array([12345], np.uint64), 2)
+    assert v[0, 0] == 0.98065389215791599 and v[0, 1] == 0.7036551539365844
+
+
+def test_sigma_max_matches_medium(scene):
+    ctx, osc = scene
+    assert ctx.sigma_max == osc.sigma_max
+
+
+def test_delta_track_fp64_parity(scene):
+    ctx, osc = scene
+    n = 200000
+    o, d, tmin, tmax = _rays(n, 7)
+    idx = np.arange(n, dtype=np.uint64) * 3 + 17
+    h_g, p_g, c_g = ctx.delta_track_batch(o, d, tmin, tmax, 99, "camera", idx, fp64=True)
+    h_o, p_o, c_o = osc.delta_track(o, d, tmin, tmax, 99, CAM, idx)
+    assert h_o.sum() > 5000
+    mism = np.count_nonzero(h_g != h_o)
+    both = (h_g == 1) & (h_o == 1)
+    same_bits = np.all(p_g[both].view(np.uint64) == p_o[both].view(np.uint64), axis=1)
+    n_diff = np.count_nonzero(~same_bits)
+    print(f"hit mismatches {mism}/{n}; position bit mismatches {n_diff}/{both.sum()}")
+    assert mism <= max(2, 1e-4 * n)
+    assert n_diff <= max(2, 1e-4 * both.sum())
+    assert np.max(np.abs(p_g[both] - p_o[both])) < 1e-12
+    ok = both & same_bits
+    assert np.array_equal(c_g[ok], c_o[ok])
+
+
+def test_delta_track_fast_statistics(scene):
+    """binary32 FAST mode: same streams; hit rate and depth distribution agree."""
+    ctx, osc = scene
+    n = 200000
+    o, d, tmin, tmax = _rays(n, 8)
+    idx = np.arange(n, dtype=np.uint64)
+    h_f, p_f, _ = ctx.delta_track_batch(o, d, tmin, tmax, 5, "camera", idx, fp64=False)
+    h_p, p_p, _ = ctx.delta_track_batch(o, d, tmin, tmax, 5, "camera", idx, fp64=True)
+    # same RNG stream positions -> almost every decision agrees (~1e-6 flips)
+    assert np.count_nonzero(h_f != h_p) <= max(20, 2e-4 * n)
+    both = (h_f == 1) & (h_p == 1)
+    err = np.abs(p_f[both] - p_p[both]).max(axis=1)
+    assert np.quantile(err, 0.999) < 1e-4
+
+
+def test_delta_track_invalid_ray(scene):
+    ctx, _ = scene
+    with pytest.raises(ValueError):
+        ctx.delta_track_batch([[np.nan, 0, 0]], [[0, 0, 1]], [0.0], [np.inf], 0, "camera", [0])
+    with pytest.raises(ValueError):
+        ctx.delta_track_batch([[0, 0, 0]], [[0, 0, 1]], [2.0], [1.0], 0, "camera", [0])
+
+
+@pytest.mark.parametrize("n_trials", [1, 4])
+def test_transmittance_parity(scene, n_trials):
+    ctx, osc = scene
+    n = 50000
+    r = np.random.default_rng(2)
+    a = r.uniform(0, 1, (n, 3))
+    b = np.tile([2.0, 2.5, -1.0], (n, 1))
+    b[::11] = a[::11]
+    idx = np.arange(n, dtype=np.uint64) * 5
+    t_g = ctx.transmittance_batch(a, b, 21, "nee", idx, n_trials)
+    t_o = osc.transmittance(a, b, 21, NEE, idx, n_trials)
+    diff = np.count_nonzero(t_g != t_o)
+    print(f"transmittance mismatches {diff}/{n}")
+    assert diff <= max(2, 1e-4 * n)
+    with pytest.raises(ValueError):
+        ctx.transmittance_batch(a[:1], b[:1], 0, "nee", idx[:1], 0)
+
+
+def test_ratio_tracking_unbiased(scene):
+    """Ratio tracking (fast mode NEE) estimates the same transmittance."""
+    ctx, osc = scene
+    r = np.random.default_rng(4)
+    a = r.uniform(0.2, 0.8, (64, 3))
+    b = np.tile([2.0, 2.5, -1.0], (64, 1))
+    idx = np.arange(64, dtype=np.uint64)
+    t_ratio = ctx.transmittance_batch(a, b, 3, "nee", idx, 20000, ratio=True)
+    t_delta = ctx.transmittance_batch(a, b, 4, "nee", idx, 20000)
+    se = np.sqrt(np.maximum(t_delta * (1 - t_delta), 1e-4) / 20000) * 2
+    assert np.all(np.abs(t_ratio - t_delta) < 5 * se + 2e-3)
