@@ -122,6 +122,9 @@ struct pf_ctx {
     // volume
     cudaArray_t vol_array = nullptr;
     cudaTextureObject_t vol_tex = 0;
+    int atlas_log2 = 0;
+    int mc[3] = {0, 0, 0};
+    DevBuf macro_mm, maj, tf_dev;
     int nx = 0, ny = 0, nz = 0;
     float vmin = 0.f, vmax = 0.f;
     // medium / lights
@@ -170,7 +173,15 @@ struct pf_ctx {
     DevScene scene() const {
         DevScene S;
         std::memset(&S, 0, sizeof(S));
-        S.vol = vol_tex;
+        S.atlas = vol_tex;
+        S.atlas_log2 = atlas_log2;
+        S.maj = (const float *)maj.p;
+        for (int a = 0; a < 3; ++a) {
+            const int n = a == 0 ? nx : a == 1 ? ny : nz;
+            S.mc[a] = mc[a];
+            S.mh[a] = (float)PF_MACRO / (float)n;
+            S.minv_h[a] = (float)n / (float)PF_MACRO;
+        }
         S.nx = nx;
         S.ny = ny;
         S.nz = nz;
@@ -308,26 +319,44 @@ int pf_volume_upload(pf_ctx *c, int nx, int ny, int nz, const float *data) {
         hi = v > hi ? v : hi;
     }
     c->free_volume();
+    // slice atlas (see DevScene): smallest power-of-two tile columns that fit
+    int max_w = 0, max_h = 0;
+    cudaDeviceGetAttribute(&max_w, cudaDevAttrMaxTexture2DWidth, c->device);
+    cudaDeviceGetAttribute(&max_h, cudaDevAttrMaxTexture2DHeight, c->device);
+    int lg = 0;
+    while ((size_t)((nz + (1 << lg) - 1) >> lg) * (size_t)(ny + 1) > (size_t)max_h) ++lg;
+    const size_t aw = (size_t)(1 << lg) * (size_t)(nx + 1);
+    const size_t ah = (size_t)((nz + (1 << lg) - 1) >> lg) * (size_t)(ny + 1);
+    if (aw > (size_t)max_w) return set_err(PF_ERR_INVALID, "VolumeGrid: %dx%dx%d exceeds the texture atlas", nx, ny, nz);
+    DevBuf lin, atl;
+    PF_CUDA(lin.ensure(n * 4));
+    PF_CUDA(atl.ensure(aw * ah * 4));
+    PF_CUDA(cudaMemcpyAsync(lin.p, src, n * 4, cudaMemcpyHostToDevice, c->stream));
+    PF_CUDA(launch_build_atlas((const float *)lin.p, nx, ny, nz, lg, (float *)atl.p, aw, ah, c->stream));
+    // FAST-mode macro-cell scalar ranges (majorants are derived per TF in pf_medium_set)
+    for (int a = 0; a < 3; ++a) c->mc[a] = ((a == 0 ? nx : a == 1 ? ny : nz) + PF_MACRO - 1) / PF_MACRO;
+    const size_t ncell = (size_t)c->mc[0] * c->mc[1] * c->mc[2];
+    PF_CUDA(c->macro_mm.ensure(ncell * sizeof(float2)));
+    PF_CUDA(c->maj.ensure(ncell * sizeof(float)));
+    PF_CUDA(launch_macro_minmax((const float *)lin.p, nx, ny, nz, (float2 *)c->macro_mm.p, c->mc[0], c->mc[1],
+                                c->mc[2], c->stream));
     cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
-    PF_CUDA(cudaMalloc3DArray(&c->vol_array, &fd, make_cudaExtent(nx, ny, nz)));
-    cudaMemcpy3DParms cp;
-    std::memset(&cp, 0, sizeof(cp));
-    cp.srcPtr = make_cudaPitchedPtr((void *)src, (size_t)nx * 4, nx, ny);
-    cp.dstArray = c->vol_array;
-    cp.extent = make_cudaExtent(nx, ny, nz);
-    cp.kind = cudaMemcpyHostToDevice;
-    PF_CUDA(cudaMemcpy3D(&cp));
+    PF_CUDA(cudaMallocArray(&c->vol_array, &fd, aw, ah));
+    PF_CUDA(cudaMemcpy2DToArrayAsync(c->vol_array, 0, 0, atl.p, aw * 4, aw * 4, ah, cudaMemcpyDeviceToDevice,
+                                     c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
     cudaResourceDesc rd;
     std::memset(&rd, 0, sizeof(rd));
     rd.resType = cudaResourceTypeArray;
     rd.res.array.array = c->vol_array;
     cudaTextureDesc td;
     std::memset(&td, 0, sizeof(td));
-    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
-    td.filterMode = cudaFilterModePoint;  // exact voxels; hardware lerp is 8-bit fixed point
+    td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModePoint;  // gathers return the stored floats; no fixed-point lerp
     td.readMode = cudaReadModeElementType;
     td.normalizedCoords = 0;
     PF_CUDA(cudaCreateTextureObject(&c->vol_tex, &rd, &td, nullptr));
+    c->atlas_log2 = lg;
     c->nx = nx;
     c->ny = ny;
     c->nz = nz;
@@ -369,6 +398,14 @@ int pf_medium_set(pf_ctx *c, const double *tf_pts, int n_pts, double density_sca
         sigma_max = density_scale * m;
     }
     c->sigma_max = sigma_max;
+    // per-macro-cell majorants for the FAST tracer
+    PF_CUDA(cudaSetDevice(c->device));
+    PF_CUDA(c->tf_dev.ensure(c->tf.size() * sizeof(double)));
+    PF_CUDA(cudaMemcpyAsync(c->tf_dev.p, c->tf.data(), c->tf.size() * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+    PF_CUDA(launch_macro_majorant((const float2 *)c->macro_mm.p, (size_t)c->mc[0] * c->mc[1] * c->mc[2],
+                                  (const double *)c->tf_dev.p, n_pts, density_scale, (float *)c->maj.p, c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));  // c->tf may be reassigned by the next call
     c->has_medium = true;
     return PF_OK;
 }
@@ -479,7 +516,7 @@ static FieldParams field_params(pf_ctx *c) {
     P.n_wg = c->f_nwg;
     P.tmem_cols = c->f_nwg <= 2 ? 128u : 256u;
     P.img_bytes = (uint32_t)h.image.size();
-    P.a_bytes = (uint32_t)(128 * h.K0 * 2);
+    P.a_bytes = 32768u;
     for (int i = 0; i < 8; ++i) P.off_w[i] = h.off_w[i];
     P.off_bias = h.off_bias;
     P.psi_log2_10 = (float)(h.psi * 3.3219280948873623478703194294894);

@@ -80,6 +80,80 @@ __global__ void k_tiles_unpack(ComposeParams C, const float *packed_all, size_t 
     dst[2] = src[2];
 }
 
+// Slice atlas for the volume texture: tile (z % cols, z / cols) holds slice z
+// with its last row / column duplicated (the reference's min(i+1, n-1) clamp).
+__global__ void k_build_atlas(const float *vol, int nx, int ny, int nz, int lg, float *atlas, size_t aw,
+                              size_t ah) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= aw * ah) return;
+    const size_t ay = i / aw, ax = i - ay * aw;
+    const int tx = (int)(ax / (size_t)(nx + 1)), ty = (int)(ay / (size_t)(ny + 1));
+    const int x = min((int)(ax - (size_t)tx * (nx + 1)), nx - 1);
+    const int y = min((int)(ay - (size_t)ty * (ny + 1)), ny - 1);
+    const int z = (ty << lg) + tx;
+    atlas[i] = z < nz ? vol[(size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * (size_t)z)] : 0.0f;
+}
+
+cudaError_t launch_build_atlas(const float *vol, int nx, int ny, int nz, int lg, float *atlas, size_t aw,
+                               size_t ah, cudaStream_t st) {
+    const size_t n = aw * ah;
+    k_build_atlas<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vol, nx, ny, nz, lg, atlas, aw, ah);
+    return cudaGetLastError();
+}
+
+// Per macro cell: min/max scalar over the voxels a trilinear sample inside
+// the cell can touch (indices [c*B-1, c*B+B], clamped).
+__global__ void k_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy, int mcz) {
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= (size_t)mcx * mcy * mcz) return;
+    const int cx = (int)(c % mcx), cy = (int)((c / mcx) % mcy), cz = (int)(c / ((size_t)mcx * mcy));
+    const int x0 = max(cx * PF_MACRO - 1, 0), x1 = min(cx * PF_MACRO + PF_MACRO, nx - 1);
+    const int y0 = max(cy * PF_MACRO - 1, 0), y1 = min(cy * PF_MACRO + PF_MACRO, ny - 1);
+    const int z0 = max(cz * PF_MACRO - 1, 0), z1 = min(cz * PF_MACRO + PF_MACRO, nz - 1);
+    float lo = 1e30f, hi = -1e30f;
+    for (int z = z0; z <= z1; ++z)
+        for (int y = y0; y <= y1; ++y)
+            for (int x = x0; x <= x1; ++x) {
+                const float v = vol[(size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * (size_t)z)];
+                lo = fminf(lo, v);
+                hi = fmaxf(hi, v);
+            }
+    mm[c] = make_float2(lo, hi);
+}
+
+// majorant = density_scale * TransferFunction::max_alpha(lo, hi) (volume.cpp:163-168), padded 1e-5.
+__device__ double tf_alpha_host_like(const double *p, int n, double s) {
+    s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+    int hi = 1;
+    while (hi + 1 < n && p[hi * 5] < s) ++hi;
+    double t = (s - p[(hi - 1) * 5]) / (p[hi * 5] - p[(hi - 1) * 5]);
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    return p[(hi - 1) * 5 + 4] + (p[hi * 5 + 4] - p[(hi - 1) * 5 + 4]) * t;
+}
+
+__global__ void k_macro_majorant(const float2 *mm, size_t ncells, const double *tf, int n, double ds, float *maj) {
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    const double lo = mm[c].x, hi = mm[c].y;
+    double m = fmax(tf_alpha_host_like(tf, n, lo), tf_alpha_host_like(tf, n, hi));
+    for (int i = 0; i < n; ++i)
+        if (tf[5 * i] > lo && tf[5 * i] < hi) m = fmax(m, tf[5 * i + 4]);
+    maj[c] = m > 0.0 ? (float)(ds * m * (1.0 + 1e-5)) : 0.0f;
+}
+
+cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy, int mcz,
+                                cudaStream_t st) {
+    const size_t n = (size_t)mcx * mcy * mcz;
+    k_macro_minmax<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(vol, nx, ny, nz, mm, mcx, mcy, mcz);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const double *tf_pts, int n_tf, double ds,
+                                  float *maj, cudaStream_t st) {
+    k_macro_majorant<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(mm, ncells, tf_pts, n_tf, ds, maj);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_compose(bool parity, const ComposeParams &C, cudaStream_t st) {
     const size_t n = (size_t)C.n_local_tiles * C.tile_w * C.tile_h;
     if (n == 0) return cudaSuccess;

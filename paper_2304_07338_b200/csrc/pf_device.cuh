@@ -25,7 +25,14 @@ constexpr double kInv4Pi = 1.0 / (4.0 * kPi);
 // ---------------------------------------------------------------- scene --
 // Passed by value as a kernel parameter (lives in the constant bank).
 struct DevScene {
-    cudaTextureObject_t vol;  // binary32 3D array, point sampling, unnormalised coords
+    // Volume "slice atlas": a 2-D binary32 texture holding every z-slice as an
+    // (nx+1) x (ny+1) tile (last row/column duplicated), 2^atlas_log2 tiles per
+    // atlas row.  One tex2Dgather returns the exact 2x2 footprint a trilinear
+    // sample needs in one slice, so a tracking step issues 2 texture
+    // instructions instead of 8 point fetches -- values are the stored floats,
+    // so results stay bit-identical to the reference's voxel() reads.
+    cudaTextureObject_t atlas;
+    int atlas_log2;
     int nx, ny, nz;
     int n_tf;
     int n_lights;
@@ -37,6 +44,14 @@ struct DevScene {
     float tf_cf[PF_MAX_TF][4];
     double light_p[PF_MAX_LIGHTS][3];
     double light_i[PF_MAX_LIGHTS][3];
+    // FAST mode only: macro-cell majorants (PF_MACRO voxels per cell edge).
+    // maj[c] >= density_scale * alpha(s) for every trilinear sample inside
+    // cell c (built from the min/max of the cell's voxel support + the TF's
+    // max_alpha, volume.cpp:163-168), so delta / ratio tracking against it is
+    // unbiased; empty cells are skipped without a texture fetch.
+    const float *maj;
+    int mc[3];
+    float mh[3], minv_h[3];
 };
 
 // ------------------------------------------------------------------ rng --
@@ -128,8 +143,17 @@ __device__ __forceinline__ float hg_eval_f(float g, float c) {
 }
 
 // ------------------------------------------------------------- volume ----
-__device__ __forceinline__ float voxel(const DevScene &S, int ix, int iy, int iz) {
-    return tex3D<float>(S.vol, (float)ix + 0.5f, (float)iy + 0.5f, (float)iz + 0.5f);
+// 2x2 footprint {(ix,iy), (ix+1,iy), (ix,iy+1), (ix+1,iy+1)} of slice iz
+// (gather component order: w=(0,0) z=(1,0) x=(0,1) y=(1,1)).
+struct Quad {
+    float c00, c10, c01, c11;
+};
+__device__ __forceinline__ Quad quad(const DevScene &S, int ix, int iy, int iz) {
+    const int mask = (1 << S.atlas_log2) - 1;
+    const float u = (float)((iz & mask) * (S.nx + 1) + ix) + 1.0f;
+    const float v = (float)((iz >> S.atlas_log2) * (S.ny + 1) + iy) + 1.0f;
+    const float4 g = tex2Dgather<float4>(S.atlas, u, v, 0);
+    return Quad{g.w, g.z, g.x, g.y};
 }
 
 // Cell-centred axis split with boundary clamp (volume.cpp:44-57).
@@ -156,11 +180,11 @@ __device__ __forceinline__ double sample_d(const DevScene &S, const double p[3])
     axis_d(p[0], S.nx, ix, fx);
     axis_d(p[1], S.ny, iy, fy);
     axis_d(p[2], S.nz, iz, fz);
-    int jx = min(ix + 1, S.nx - 1), jy = min(iy + 1, S.ny - 1), jz = min(iz + 1, S.nz - 1);
-    double c000 = voxel(S, ix, iy, iz), c100 = voxel(S, jx, iy, iz);
-    double c010 = voxel(S, ix, jy, iz), c110 = voxel(S, jx, jy, iz);
-    double c001 = voxel(S, ix, iy, jz), c101 = voxel(S, jx, iy, jz);
-    double c011 = voxel(S, ix, jy, jz), c111 = voxel(S, jx, jy, jz);
+    const int jz = min(iz + 1, S.nz - 1);
+    const Quad q0 = quad(S, ix, iy, iz), q1 = quad(S, ix, iy, jz);
+    // jx/jy = min(i+1, n-1) come from the duplicated tile edge
+    double c000 = q0.c00, c100 = q0.c10, c010 = q0.c01, c110 = q0.c11;
+    double c001 = q1.c00, c101 = q1.c10, c011 = q1.c01, c111 = q1.c11;
     double c00 = c000 * (1.0 - fx) + c100 * fx;
     double c10 = c010 * (1.0 - fx) + c110 * fx;
     double c01 = c001 * (1.0 - fx) + c101 * fx;
@@ -192,11 +216,10 @@ __device__ __forceinline__ float sample_f(const DevScene &S, const float p[3]) {
     axis_f(p[0], S.nx, ix, fx);
     axis_f(p[1], S.ny, iy, fy);
     axis_f(p[2], S.nz, iz, fz);
-    int jx = min(ix + 1, S.nx - 1), jy = min(iy + 1, S.ny - 1), jz = min(iz + 1, S.nz - 1);
-    float c000 = voxel(S, ix, iy, iz), c100 = voxel(S, jx, iy, iz);
-    float c010 = voxel(S, ix, jy, iz), c110 = voxel(S, jx, jy, iz);
-    float c001 = voxel(S, ix, iy, jz), c101 = voxel(S, jx, iy, jz);
-    float c011 = voxel(S, ix, jy, jz), c111 = voxel(S, jx, jy, jz);
+    const int jz = min(iz + 1, S.nz - 1);
+    const Quad q0 = quad(S, ix, iy, iz), q1 = quad(S, ix, iy, jz);
+    const float c000 = q0.c00, c100 = q0.c10, c010 = q0.c01, c110 = q0.c11;
+    const float c001 = q1.c00, c101 = q1.c10, c011 = q1.c01, c111 = q1.c11;
     float c00 = c000 + (c100 - c000) * fx;
     float c10 = c010 + (c110 - c010) * fx;
     float c01 = c001 + (c101 - c001) * fx;

@@ -151,17 +151,24 @@ __device__ __forceinline__ void issue_layer(uint32_t a_s, uint32_t b_s, int K, i
     }
 }
 
+// Zero-pad columns [k0, k1) of row r in a chunk tile of width W (multiples of 8).
+__device__ __forceinline__ void zero_cols(uint8_t *A, int r, int k0, int k1, uint32_t sbo) {
+    for (int k = k0; k < k1; k += 8)
+        *reinterpret_cast<uint4 *>(A + (r >> 3) * sbo + (k >> 3) * 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+}
+
 template <int FP, int FD>
 __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *img = smem;
     uint8_t *abase = smem + P.img_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(abase + (size_t)P.n_wg * P.a_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + P.n_wg);
+    // per warpgroup: two 128 x 64 fp16 chunk tiles (16 KB each) + 2 mbarriers
+    uint64_t *bars = reinterpret_cast<uint64_t *>(abase + (size_t)P.n_wg * 32768);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + 2 * P.n_wg);
 
     const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5;
     if (tid == 0) {
-        for (int i = 0; i <= P.n_wg; ++i) mbar_init(smem_u32(&bars[i]), 1);
+        for (int i = 0; i <= 2 * P.n_wg; ++i) mbar_init(smem_u32(&bars[i]), 1);
         mbar_fence_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), P.tmem_cols);
@@ -177,17 +184,29 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
 
     const size_t n_items = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
     const size_t n_tiles = (n_items + 127) / 128;
-    uint8_t *A = abase + (size_t)wg * P.a_bytes;
-    const uint32_t a_s = smem_u32(A), img_s = smem_u32(img);
+    uint8_t *buf[2] = {abase + (size_t)wg * 32768, abase + (size_t)wg * 32768 + 16384};
+    const uint32_t buf_s[2] = {smem_u32(buf[0]), smem_u32(buf[1])};
+    const uint32_t img_s = smem_u32(img);
     const uint32_t tmem_wg = tmem_base + (uint32_t)(wg * 64);
     const uint32_t tmem_rows = tmem_wg + ((uint32_t)(32 * (warp & 3)) << 16);
-    const uint32_t mbar = smem_u32(&bars[1 + wg]);
-    const uint32_t sbo0 = (uint32_t)P.K0 * 16u;
+    const uint32_t mbar[2] = {smem_u32(&bars[1 + 2 * wg]), smem_u32(&bars[2 + 2 * wg])};
+    uint32_t ph[2] = {0u, 0u};
+    bool pending[2] = {false, false};
     const float *bias = reinterpret_cast<const float *>(img + P.off_bias);
-    uint32_t phase = 0;
+    const int kdir = P.n_pos_levels * FP;
+    const int kg = kdir + P.n_dir_levels * FD;     // column of the g input
+    const int nch = (P.K0 + 63) / 64;
+    const uint32_t sbo_w0 = (uint32_t)P.K0 * 16u;
 
-    for (size_t tile = (size_t)blockIdx.x * P.n_wg + wg; tile < n_tiles;
-         tile += (size_t)gridDim.x * P.n_wg) {
+    auto wait_buf = [&](int b) {
+        if (pending[b]) {
+            mbar_wait(mbar[b], ph[b]);
+            ph[b] ^= 1u;
+            pending[b] = false;
+        }
+    };
+
+    for (size_t tile = (size_t)blockIdx.x * P.n_wg + wg; tile < n_tiles; tile += (size_t)gridDim.x * P.n_wg) {
         const size_t row = tile * 128 + r;
         const bool valid = row < n_items;
         float x[3] = {0.f, 0.f, 0.f}, ws[2] = {0.f, 0.f}, gin = 0.f;
@@ -213,35 +232,53 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
                 gin = P.qg[row];
             }
         }
-        // ---- K3: encode straight into the A tile (layer-0 layout, K = K0)
-        encode_grid<3, FP>(P, 0, P.n_pos_levels, x, A, r, 0, sbo0);
-        const int kdir = P.n_pos_levels * FP;
-        encode_grid<2, FD>(P, P.n_pos_levels, P.n_dir_levels, ws, A, r, kdir, sbo0);
-        {
-            const int kg = kdir + P.n_dir_levels * FD;  // multiple of 8 (checked on host)
-            uint8_t *p = A + (r >> 3) * sbo0 + (kg >> 3) * 128 + (r & 7) * 16;
-            uint4 u = make_uint4(0u, 0u, 0u, 0u);
-            __half gh = __float2half_rn((gin + 1.0f) * 0.5f);
-            u.x = (uint32_t)__half_as_ushort(gh);
-            *reinterpret_cast<uint4 *>(p) = u;
-            for (int kk = kg + 8; kk < P.K0; kk += 8)
-                *reinterpret_cast<uint4 *>(A + (r >> 3) * sbo0 + (kk >> 3) * 128 + (r & 7) * 16) =
-                    make_uint4(0u, 0u, 0u, 0u);
+        // ---- K3 + layer-0 MMA, chunk by chunk (encode j+1 overlaps MMA j)
+        for (int j = 0; j < nch; ++j) {
+            const int b = j & 1;
+            const int k0 = 64 * j, kw = min(64, P.K0 - k0);
+            const uint32_t sbo = (uint32_t)kw * 16u;
+            wait_buf(b);  // the MMA that last read this buffer is done
+            uint8_t *A = buf[b];
+            // position levels whose features start in [k0, k0+kw)
+            const int lp0 = min(P.n_pos_levels, k0 / FP), lp1 = min(P.n_pos_levels, (k0 + kw) / FP);
+            if (lp1 > lp0) encode_grid<3, FP>(P, lp0, lp1 - lp0, x, A, r, lp0 * FP - k0, sbo);
+            const int ld0 = min(P.n_dir_levels, max(0, (k0 - kdir + FD - 1) / FD));
+            const int ld1 = min(P.n_dir_levels, max(0, (k0 + kw - kdir + FD - 1) / FD));
+            if (ld1 > ld0) encode_grid<2, FD>(P, P.n_pos_levels + ld0, ld1 - ld0, ws, A, r, kdir + ld0 * FD - k0, sbo);
+            if (kg >= k0 && kg < k0 + kw) {
+                const int kk = kg - k0;
+                uint8_t *p = A + (r >> 3) * sbo + (kk >> 3) * 128 + (r & 7) * 16;
+                uint4 u = make_uint4(0u, 0u, 0u, 0u);
+                u.x = (uint32_t)__half_as_ushort(__float2half_rn((gin + 1.0f) * 0.5f));
+                *reinterpret_cast<uint4 *>(p) = u;
+                zero_cols(A, r, kk + 8, kw, sbo);
+            } else if (kg < k0) {
+                zero_cols(A, r, 0, kw, sbo);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1 + wg, 128);
+            if (r == 0) {
+                tc_fence_after();
+                const uint32_t idesc = umma_idesc_f16(128, 64);
+                for (int s = 0; s < kw / 16; ++s) {
+                    const uint64_t ad = umma_sdesc(buf_s[b] + 256u * s, 128u, sbo);
+                    const uint64_t bd = umma_sdesc(img_s + P.off_w[0] + (uint32_t)(k0 / 8) * 128u + 256u * s, 128u,
+                                                   sbo_w0);
+                    umma_f16(tmem_wg, ad, bd, idesc, (j > 0 || s > 0) ? 1u : 0u);
+                }
+                umma_commit(mbar[b]);
+            }
+            pending[b] = true;
         }
-        fence_proxy_async_smem();
-        named_bar_sync(1 + wg, 128);
-        if (r == 0) {
-            tc_fence_after();
-            issue_layer(a_s, img_s + P.off_w[0], P.K0, 64, tmem_wg);
-            umma_commit(mbar);
-        }
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
+        wait_buf(0);
+        wait_buf(1);
         tc_fence_after();
 
-        // ---- K4: hidden layers (epilogue of layer L-1 feeds MMA of layer L)
+        // ---- K4: hidden layers (epilogue of layer L-1 feeds the MMA of layer L)
         for (int L = 1; L <= P.hidden_layers; ++L) {
-            const float *b = bias + (L - 1) * 64;
+            const int b = L & 1;
+            uint8_t *A = buf[b];
+            const float *bl = bias + (L - 1) * 64;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 float v[16];
@@ -251,12 +288,11 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
                 __half2 *h = reinterpret_cast<__half2 *>(u);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const float a0 = fmaxf(v[2 * i] + b[16 * c + 2 * i], 0.f);
-                    const float a1 = fmaxf(v[2 * i + 1] + b[16 * c + 2 * i + 1], 0.f);
+                    const float a0 = fmaxf(v[2 * i] + bl[16 * c + 2 * i], 0.f);
+                    const float a1 = fmaxf(v[2 * i + 1] + bl[16 * c + 2 * i + 1], 0.f);
                     h[i] = __floats2half2_rn(a0, a1);
                 }
-                // K = 64 layout: SBO = 1024
-                uint8_t *p = A + (r >> 3) * 1024 + (2 * c) * 128 + (r & 7) * 16;
+                uint8_t *p = A + (r >> 3) * 1024 + (2 * c) * 128 + (r & 7) * 16;  // K = 64: SBO = 1024
                 *reinterpret_cast<uint4 *>(p) = u[0];
                 *reinterpret_cast<uint4 *>(p + 128) = u[1];
             }
@@ -265,11 +301,11 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
             named_bar_sync(1 + wg, 128);
             if (r == 0) {
                 tc_fence_after();
-                issue_layer(a_s, img_s + P.off_w[L], 64, L < P.hidden_layers ? 64 : 16, tmem_wg);
-                umma_commit(mbar);
+                issue_layer(buf_s[b], img_s + P.off_w[L], 64, L < P.hidden_layers ? 64 : 16, tmem_wg);
+                umma_commit(mbar[b]);
             }
-            mbar_wait(mbar, phase);
-            phase ^= 1u;
+            pending[b] = true;
+            wait_buf(b);
             tc_fence_after();
         }
 
@@ -286,18 +322,17 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
                 for (int c = 0; c < 3; ++c) {
                     const float Li = exp2f(-__saturatef(o3[c]) * P.psi_log2_10);  // Eq. 8
                     if (P.slot_f64) {
-                        double *s = reinterpret_cast<double *>(P.slots) + 3 * (size_t)slot + c;
-                        *s = *s + P.w_i * (sigma_s * (double)Li);
+                        double *sp = reinterpret_cast<double *>(P.slots) + 3 * (size_t)slot + c;
+                        *sp = *sp + P.w_i * (sigma_s * (double)Li);
                     } else {
-                        float *s = reinterpret_cast<float *>(P.slots) + 3 * (size_t)slot + c;
-                        *s = *s + (float)P.w_i * ((float)sigma_s * Li);
+                        float *sp = reinterpret_cast<float *>(P.slots) + 3 * (size_t)slot + c;
+                        *sp = *sp + (float)P.w_i * ((float)sigma_s * Li);
                     }
                 }
             } else {
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
-                    P.qout[3 * row + c] =
-                        P.decoded ? exp2f(-__saturatef(o3[c]) * P.psi_log2_10) : o3[c];
+                    P.qout[3 * row + c] = P.decoded ? exp2f(-__saturatef(o3[c]) * P.psi_log2_10) : o3[c];
             }
         }
     }
@@ -359,8 +394,8 @@ const char *field_validate(const FieldDesc &d) {
         if (g->log2_table < 4 || g->log2_table > 24) return "field: log2_table in [4,24]";
         if (level_res(*g, g->levels - 1) > (1 << 24)) return "field: level resolution too large";
     }
-    if ((d.pos.levels * d.pos.features + d.dir.levels * d.dir.features) % 8 != 0)
-        return "field: levels*features (pos + dir) must be a multiple of 8";
+    if ((d.pos.levels * d.pos.features) % 8 != 0 || (d.dir.levels * d.dir.features) % 8 != 0)
+        return "field: levels*features must be a multiple of 8 for each grid";
     if (!(d.psi > 0.0)) return "field: psi must be positive";
     return nullptr;
 }
@@ -436,15 +471,15 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
 int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, int device) {
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    const size_t a_bytes = (size_t)128 * h.K0 * 2;
+    const size_t per_wg = 32768;  // two 128 x 64 fp16 chunk tiles
     const size_t fixed = h.image.size() + 256;
     n_wg = 0;
     for (int k = 4; k >= 1; --k)
-        if (fixed + k * a_bytes <= (size_t)max_smem) {
+        if (fixed + k * per_wg <= (size_t)max_smem) {
             n_wg = k;
             break;
         }
-    smem = fixed + (size_t)n_wg * a_bytes;
+    smem = fixed + (size_t)n_wg * per_wg;
     return n_wg > 0 ? 0 : 1;
 }
 

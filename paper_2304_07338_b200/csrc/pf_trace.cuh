@@ -369,52 +369,5 @@ __global__ void k_rng_doubles(BatchParams B) {
 
 #endif  // PF_TU_PARITY
 
-#ifdef PF_TU_FAST
-// Ratio tracking (FAST mode shadow estimator, binary32), averaged over trials.
-__global__ void k_transmittance_ratio_batch(const DevScene S, BatchParams B) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B.n) return;
-    Pcg rng;
-    pcg_init(rng, B.initstate, B.idx[i]);
-    float a[3], dv[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        a[k] = (float)B.a3[3 * i + k];
-        dv[k] = (float)B.b3[3 * i + k] - a[k];
-    }
-    const float len = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
-    if (len == 0.0f) {
-        B.out[i] = 1.0;
-        return;
-    }
-    float dir[3] = {dv[0] / len, dv[1] / len, dv[2] / len};
-    float t0, t1;
-    if (!aabb_unit<float>(a, dir, 0.0f, len, t0, t1) || !(S.sigma_max_f > 0.0f)) {
-        B.out[i] = 1.0;
-        return;
-    }
-    double acc = 0.0;
-    for (int trial = 0; trial < B.n_trials; ++trial) {
-        float t = t0, T = 1.0f;
-        for (;;) {
-            t -= __logf(pcg_one_minus_u_f(rng)) * S.inv_sigma_max_f;
-            if (t > t1) break;
-            float x[3] = {a[0] + dir[0] * t, a[1] + dir[1] * t, a[2] + dir[2] * t};
-            const float sigma = S.density_scale_f * tf_alpha_f(S, sample_f(S, x));
-            T *= 1.0f - sigma * S.inv_sigma_max_f;
-            if (T < 0.1f) {
-                if (pcg_u_f(rng) >= T * 10.0f) {
-                    T = 0.0f;
-                    break;
-                }
-                T = 0.1f;
-            }
-        }
-        acc += (double)T;
-    }
-    B.out[i] = acc / B.n_trials;
-}
-
-#endif  // PF_TU_FAST
 
 }  // namespace pfk

@@ -1,34 +1,325 @@
-// pf_trace_fast.cu -- binary32 FAST instantiation of pf_trace.cuh (ratio-
-// tracked shadow rays).  Same RNG streams as the parity path.
+// pf_trace_fast.cu -- FAST-mode render tracer (binary32) + fast batch entries.
+//
+// Same persistent lane state machine and the same per-sample RNG streams as
+// the parity tracer (pf_trace.cuh), but the majorant is piecewise constant
+// over PF_MACRO^3-voxel macro cells instead of the reference's single global
+// sigma_max (volume.cpp:197-202):
+//   * a flight samples an optical depth tau = -log(1-u) and walks the macro
+//     grid with a 3-D DDA, spending tau at rate maj[cell] -- empty cells cost
+//     a few ALU ops and no texture fetch;
+//   * at a tentative collision in cell c the primary ray accepts with
+//     probability sigma(x) / maj[c] (delta tracking), a shadow ray multiplies
+//     its transmittance by 1 - sigma(x) / maj[c] (ratio tracking, north_star)
+//     with Russian roulette below 0.1.
+// Both estimators stay unbiased for any majorant >= sigma, so the FAST frame
+// converges to the PARITY frame (statistical parity, tests/test_gpu_render.py);
+// the RNG stream of a sample is consumed differently, so single samples differ.
 #define PF_TU_FAST
 #include "pf_trace.cuh"
 
 namespace pfk {
 
-cudaError_t launch_render_trace_fast(const DevScene &S, const TraceParams &P, int grid,
-                                     cudaStream_t st) {
-    k_render_trace<false><<<grid, PF_TRACE_THREADS, 0, st>>>(S, P);
+struct Dda {
+    int c[3];        // current macro cell
+    int step[3];     // +1 / -1
+    float tm[3];     // ray parameter of the next boundary crossing per axis
+    float td[3];     // parameter increment per cell per axis
+};
+
+__device__ __forceinline__ void dda_init(const DevScene &S, const float o[3], const float d[3], float t, Dda &D) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float p = fmaf(d[a], t, o[a]);
+        int ci = (int)floorf(p * S.minv_h[a]);
+        ci = min(max(ci, 0), S.mc[a] - 1);
+        D.c[a] = ci;
+        const float inv = 1.0f / d[a];  // +-inf for axis-parallel rays
+        if (d[a] > 0.0f) {
+            D.step[a] = 1;
+            D.tm[a] = ((float)(ci + 1) * S.mh[a] - o[a]) * inv;
+            D.td[a] = S.mh[a] * inv;
+        } else if (d[a] < 0.0f) {
+            D.step[a] = -1;
+            D.tm[a] = ((float)ci * S.mh[a] - o[a]) * inv;
+            D.td[a] = -S.mh[a] * inv;
+        } else {
+            D.step[a] = 0;
+            D.tm[a] = __int_as_float(0x7f800000);
+            D.td[a] = __int_as_float(0x7f800000);
+        }
+    }
+}
+
+// Spend optical depth tau through the majorant grid from t.  Returns true at a
+// tentative collision (t updated, m = that cell's majorant); false when the
+// flight reaches t1 first.
+__device__ __forceinline__ bool dda_advance(const DevScene &S, Dda &D, float &t, float t1, float &tau, float &m) {
+    for (;;) {
+        const int cell = D.c[0] + S.mc[0] * (D.c[1] + S.mc[1] * D.c[2]);
+        m = __ldg(S.maj + cell);
+        const int ax = (D.tm[0] < D.tm[1]) ? (D.tm[0] < D.tm[2] ? 0 : 2) : (D.tm[1] < D.tm[2] ? 1 : 2);
+        const float t_exit = fminf(D.tm[ax], t1);
+        const float seg = t_exit - t;
+        const float od = m * seg;
+        if (od >= tau && m > 0.0f) {
+            t += tau / m;
+            return true;
+        }
+        tau -= od;
+        t = t_exit;
+        if (t_exit >= t1) return false;
+        D.c[ax] += D.step[ax];
+        if (D.c[ax] < 0 || D.c[ax] >= S.mc[ax]) return false;
+        D.tm[ax] += D.td[ax];
+    }
+}
+
+__device__ __forceinline__ float sample_tau(Pcg &r) { return -__logf(pcg_one_minus_u_f(r)); }
+
+__global__ void __launch_bounds__(PF_TRACE_THREADS) k_render_trace_fast(const DevScene S, const TraceParams P) {
+    float *slots = reinterpret_cast<float *>(P.slots);
+    const float ds = S.density_scale_f;
+    const float g = (float)P.g;
+
+    int phase = 0;  // 0 fetch, 1 primary flight, 2 shadow flight
+    uint32_t w = 0;
+    uint64_t index = 0;
+    Pcg rng;
+    float o[3], d[3], wo[3], t = 0.f, t1 = 0.f, tau = 0.f, T = 1.f;
+    float rgba[4], Ld[3];
+    Dda D;
+    int light = 0;
+    uint32_t nprim = 0, nshad = 0;
+
+    for (;;) {
+        if (phase == 0) {
+            w = (uint32_t)warp_fetch_add(&P.counters[0], 1u);
+            if (w >= P.n_work) break;
+            int px, py;
+            if (!decode_work(P, w, px, py, index)) continue;
+            pcg_init(rng, P.init_cam, index);
+            const float u = (float)pcg_double(rng);
+            const float v = (float)pcg_double(rng);
+            const float sx = (2.0f * ((float)px + u)) / (float)P.W - 1.0f;
+            const float sy = 1.0f - (2.0f * ((float)py + v)) / (float)P.H;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                o[a] = (float)P.cam_o[a];
+                d[a] = ((float)P.cam_f[a] + (float)P.cam_r[a] * sx) + (float)P.cam_u[a] * sy;
+            }
+            const float rl = rsqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                d[a] *= rl;
+                wo[a] = -d[a];
+            }
+            float t0;
+            if (!aabb_unit<float>(o, d, 0.0f, __int_as_float(0x7f800000), t0, t1) || !(S.sigma_max_f > 0.0f)) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = (float)P.bg[c];
+                continue;
+            }
+            t = t0;
+            dda_init(S, o, d, t, D);
+            tau = sample_tau(rng);
+            phase = 1;
+        }
+
+        // ---- advance to the next tentative collision (majorant DDA)
+        float m;
+        const bool coll = dda_advance(S, D, t, t1, tau, m);
+        if (phase == 1) ++nprim;
+        else ++nshad;
+
+        bool flight_done = false;
+        if (!coll) {
+            if (phase == 1) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = (float)P.bg[c];
+                phase = 0;
+                continue;
+            }
+            flight_done = true;
+        } else {
+            float x[3] = {fmaf(d[0], t, o[0]), fmaf(d[1], t, o[1]), fmaf(d[2], t, o[2])};
+            const float scalar = sample_f(S, x);
+            const float sigma = ds * tf_alpha_f(S, scalar);
+            if (phase == 1) {
+                if (pcg_u_f(rng) * m < sigma) {
+                    tf_rgba_f(S, scalar, rgba);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        o[a] = x[a];
+                        Ld[a] = 0.f;
+                    }
+                    pcg_init(rng, P.init_nee, index);
+                    light = -1;
+                    flight_done = true;
+                    T = 1.f;
+                    phase = 2;
+                } else {
+                    tau = sample_tau(rng);
+                }
+            } else {
+                T *= 1.0f - sigma / m;
+                if (T < 0.1f) {
+                    if (pcg_u_f(rng) >= T * 10.0f) {
+                        T = 0.f;
+                        flight_done = true;
+                    } else {
+                        T = 0.1f;
+                    }
+                }
+                if (!flight_done) tau = sample_tau(rng);
+            }
+        }
+        if (!flight_done) continue;
+
+        if (light >= 0) nee_term<float>(S, light, o, wo, g, T, Ld);
+        for (;;) {
+            ++light;
+            if (light >= S.n_lights) break;
+            float dv[3] = {(float)S.light_p[light][0] - o[0], (float)S.light_p[light][1] - o[1],
+                           (float)S.light_p[light][2] - o[2]};
+            const float len = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+            if (len > 0.0f) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) d[a] = dv[a] / len;
+                float a0, a1;
+                if (aabb_unit<float>(o, d, 0.0f, len, a0, a1) && S.sigma_max_f > 0.0f) {
+                    t = a0;
+                    t1 = a1;
+                    T = 1.f;
+                    dda_init(S, o, d, t, D);
+                    tau = sample_tau(rng);
+                    break;
+                }
+            }
+            nee_term<float>(S, light, o, wo, g, 1.0f, Ld);
+        }
+        if (light < S.n_lights) continue;
+
+        const size_t sb = 3 * (size_t)w;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) slots[sb + c] = (float)P.w_d * Ld[c];
+        const unsigned long long h = warp_fetch_add(&P.counters[1], 1u);
+        if (P.use_field) {
+            HitRec rec;
+            rec.x[0] = o[0];
+            rec.x[1] = o[1];
+            rec.x[2] = o[2];
+            const float wz = fminf(fmaxf(wo[2], -1.0f), 1.0f);
+            rec.wsph[0] = acosf(wz) * (float)(1.0 / kPi);
+            rec.wsph[1] = (atan2f(wo[1], wo[0]) + (float)kPi) * (float)(0.5 / kPi);
+            rec.slot = w;
+            rec.sigma_s = (double)(rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) * (1.0f / 3.0f)));
+            P.hits[h] = rec;
+        }
+        phase = 0;
+    }
+    atomicAdd(&P.counters[2], (unsigned long long)nprim);
+    atomicAdd(&P.counters[3], (unsigned long long)nshad);
+}
+
+cudaError_t launch_render_trace_fast(const DevScene &S, const TraceParams &P, int grid, cudaStream_t st) {
+    k_render_trace_fast<<<grid, PF_TRACE_THREADS, 0, st>>>(S, P);
     return cudaGetLastError();
 }
 
-cudaError_t launch_delta_track_batch_fast(const DevScene &S, const BatchParams &B,
-                                          cudaStream_t st) {
+// FAST-mode batch entries (DDA majorants): what the render tracer does per
+// flight, exposed for statistical tests against the parity kernels.
+__global__ void k_delta_track_batch_dda(const DevScene S, BatchParams B) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.n) return;
+    Pcg rng;
+    pcg_init(rng, B.initstate, B.idx[i]);
+    float o[3], d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        o[a] = (float)B.a3[3 * i + a];
+        d[a] = (float)B.b3[3 * i + a];
+    }
+    float t, t1;
+    B.hit[i] = 0;
+    if (!aabb_unit<float>(o, d, (float)B.tmin[i], (float)B.tmax[i], t, t1) || !(S.sigma_max_f > 0.f)) return;
+    Dda D;
+    dda_init(S, o, d, t, D);
+    float tau = sample_tau(rng), m;
+    while (dda_advance(S, D, t, t1, tau, m)) {
+        float x[3] = {fmaf(d[0], t, o[0]), fmaf(d[1], t, o[1]), fmaf(d[2], t, o[2])};
+        const float s = sample_f(S, x);
+        if (pcg_u_f(rng) * m < S.density_scale_f * tf_alpha_f(S, s)) {
+            B.hit[i] = 1;
+            if (B.pos3)
+                for (int a = 0; a < 3; ++a) B.pos3[3 * i + a] = (double)x[a];
+            if (B.rgba4) {
+                float c[4];
+                tf_rgba_f(S, s, c);
+                for (int a = 0; a < 4; ++a) B.rgba4[4 * i + a] = (double)c[a];
+            }
+            return;
+        }
+        tau = sample_tau(rng);
+    }
+}
+
+__global__ void k_transmittance_ratio_dda(const DevScene S, BatchParams B) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.n) return;
+    Pcg rng;
+    pcg_init(rng, B.initstate, B.idx[i]);
+    float a[3], dv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a[k] = (float)B.a3[3 * i + k];
+        dv[k] = (float)B.b3[3 * i + k] - a[k];
+    }
+    const float len = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+    float dir[3] = {dv[0] / len, dv[1] / len, dv[2] / len};
+    float t0, t1;
+    if (len == 0.0f || !aabb_unit<float>(a, dir, 0.0f, len, t0, t1) || !(S.sigma_max_f > 0.0f)) {
+        B.out[i] = 1.0;
+        return;
+    }
+    double acc = 0.0;
+    for (int trial = 0; trial < B.n_trials; ++trial) {
+        float t = t0, T = 1.0f, m;
+        Dda D;
+        dda_init(S, a, dir, t, D);
+        float tau = sample_tau(rng);
+        while (dda_advance(S, D, t, t1, tau, m)) {
+            float x[3] = {fmaf(dir[0], t, a[0]), fmaf(dir[1], t, a[1]), fmaf(dir[2], t, a[2])};
+            T *= 1.0f - S.density_scale_f * tf_alpha_f(S, sample_f(S, x)) / m;
+            if (T < 0.1f) {
+                if (pcg_u_f(rng) >= T * 10.0f) {
+                    T = 0.0f;
+                    break;
+                }
+                T = 0.1f;
+            }
+            tau = sample_tau(rng);
+        }
+        acc += (double)T;
+    }
+    B.out[i] = acc / B.n_trials;
+}
+
+cudaError_t launch_delta_track_batch_fast(const DevScene &S, const BatchParams &B, cudaStream_t st) {
     const unsigned blocks = (unsigned)((B.n + 127) / 128);
-    k_delta_track_batch<false><<<blocks, 128, 0, st>>>(S, B);
+    k_delta_track_batch_dda<<<blocks, 128, 0, st>>>(S, B);
     return cudaGetLastError();
 }
 
-cudaError_t launch_transmittance_ratio_batch(const DevScene &S, const BatchParams &B,
-                                             cudaStream_t st) {
+cudaError_t launch_transmittance_ratio_batch(const DevScene &S, const BatchParams &B, cudaStream_t st) {
     const unsigned blocks = (unsigned)((B.n + 127) / 128);
-    k_transmittance_ratio_batch<<<blocks, 128, 0, st>>>(S, B);
+    k_transmittance_ratio_dda<<<blocks, 128, 0, st>>>(S, B);
     return cudaGetLastError();
 }
 
 int trace_grid_size_fast(int device) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_trace<false>, PF_TRACE_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_trace_fast, PF_TRACE_THREADS, 0);
     return sms * (per_sm > 0 ? per_sm : 1);
 }
 

@@ -1,0 +1,100 @@
+"""Multi-GPU image-tile sharding.
+
+One process per GPU.  Screen tiles (tile_w x tile_h) are numbered row-major
+and interleaved round-robin over the ranks (tile t -> rank t % world), so
+screen-space load imbalance averages out and every rank's tile list is static.
+Every camera sample owns the RNG stream make_rng(seed, stream, global sample
+index), hence the frame is byte-identical for any world size.  Per frame:
+  1. each rank renders only its tiles (pf_render_neural with shard_index /
+     shard_count) into a local frame buffer;
+  2. it packs its tiles contiguously (pf_tiles_pack) into a buffer padded to
+     the largest shard's tile count;
+  3. one all_gather_into_tensor (NCCL over NVLink/NVSwitch) moves the packed
+     tiles; rank 0 de-tiles them into the final frame (pf_tiles_unpack).
+The functions below are the host-side statement of that tile map -- the CUDA
+kernels implement the same arithmetic -- and a CPU/gloo implementation of the
+exchange used to test the N > 1 logic without GPUs.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def tile_grid(width: int, height: int, tile_w: int, tile_h: int) -> tuple[int, int]:
+    return (width + tile_w - 1) // tile_w, (height + tile_h - 1) // tile_h
+
+
+def shard_tiles(width, height, tile_w, tile_h, shard, count) -> list[int]:
+    tx, ty = tile_grid(width, height, tile_w, tile_h)
+    return list(range(shard, tx * ty, count))
+
+
+def tile_rect(t, width, height, tile_w, tile_h) -> tuple[int, int, int, int]:
+    tx, _ = tile_grid(width, height, tile_w, tile_h)
+    x0, y0 = (t % tx) * tile_w, (t // tx) * tile_h
+    return x0, y0, min(x0 + tile_w, width), min(y0 + tile_h, height)
+
+
+def packed_floats(width, height, tile_w, tile_h, count) -> int:
+    """Per-shard packed buffer length (padded to the largest shard)."""
+    tx, ty = tile_grid(width, height, tile_w, tile_h)
+    return ((tx * ty + count - 1) // count) * tile_w * tile_h * 3
+
+
+def pack_tiles(frame, width, height, tile_w, tile_h, shard, count, out=None):
+    """Host statement of pf_tiles_pack: tile-major, row-major inside a tile, zero padding."""
+    import torch
+    per = packed_floats(width, height, tile_w, tile_h, count)
+    out = torch.zeros(per, dtype=torch.float32) if out is None else out
+    view = out.view(-1, tile_h, tile_w, 3)
+    for j, t in enumerate(shard_tiles(width, height, tile_w, tile_h, shard, count)):
+        x0, y0, x1, y1 = tile_rect(t, width, height, tile_w, tile_h)
+        view[j, : y1 - y0, : x1 - x0] = frame[y0:y1, x0:x1]
+    return out
+
+
+def unpack_tiles(packed_all, width, height, tile_w, tile_h, count, frame):
+    """Host statement of pf_tiles_unpack."""
+    per = packed_floats(width, height, tile_w, tile_h, count)
+    for r in range(count):
+        view = packed_all[r * per:(r + 1) * per].view(-1, tile_h, tile_w, 3)
+        for j, t in enumerate(shard_tiles(width, height, tile_w, tile_h, r, count)):
+            x0, y0, x1, y1 = tile_rect(t, width, height, tile_w, tile_h)
+            frame[y0:y1, x0:x1] = view[j, : y1 - y0, : x1 - x0]
+    return frame
+
+
+def gather_frame_host(local_frame, width, height, tile_w, tile_h, group=None):
+    """The N > 1 exchange on host tensors (gloo): pack -> all_gather -> unpack on rank 0."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    packed = pack_tiles(local_frame, width, height, tile_w, tile_h, rank, world)
+    gathered = torch.empty(packed.numel() * world, dtype=torch.float32)
+    dist.all_gather_into_tensor(gathered, packed, group=group)
+    if rank != 0:
+        return None
+    frame = torch.zeros((height, width, 3), dtype=torch.float32)
+    return unpack_tiles(gathered, width, height, tile_w, tile_h, world, frame)
+
+
+def render_frame_sharded(ctx, cam, rc, frame, packed, gathered, group=None):
+    """Device path used by bench.py: render own tiles, NCCL all_gather, rank-0 de-tile."""
+    import torch.distributed as dist
+    ctx.render_neural(cam, rc, out=frame)
+    if rc.shard_count == 1:
+        return frame
+    ctx.tiles_pack(cam, rc, frame, packed)
+    dist.all_gather_into_tensor(gathered, packed, group=group)
+    if rc.shard_index == 0:
+        ctx.tiles_unpack(cam, rc, gathered, packed.numel(), frame)
+    return frame
+
+
+def _check_cover(width, height, tile_w, tile_h, count) -> bool:
+    seen = np.zeros((height, width), np.int32)
+    for s in range(count):
+        for t in shard_tiles(width, height, tile_w, tile_h, s, count):
+            x0, y0, x1, y1 = tile_rect(t, width, height, tile_w, tile_h)
+            seen[y0:y1, x0:x1] += 1
+    return bool(np.all(seen == 1))

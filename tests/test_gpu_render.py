@@ -6,8 +6,9 @@ Tolerances:
     bit differently from glibc -> <= 1e-3 of pixels differ, none by > 1e-5 rel.
   * PARITY mode, L_i on: the field runs in fp16/fp32 (test_gpu_field), so the
     frame must agree to per-pixel RMSE <= 2e-3 * mean radiance + 1e-6.
-  * FAST mode (binary32 + ratio tracking): statistical -- a 64-spp frame
-    agrees with the 64-spp parity frame to relative RMSE <= 5%.
+  * FAST mode (binary32, macro-cell majorant DDA, ratio-tracked NEE): it
+    consumes its RNG streams differently, so it is statistical -- frame means
+    within 1.5% and per-pixel RMSE <= 1.2x the parity-vs-parity noise floor.
   * Shard/tiling invariance is exact (byte-identical) in both modes.
 """
 import numpy as np
@@ -61,13 +62,19 @@ def test_parity_with_field_matches_oracle(config1, oracle):
 
 
 def test_fast_mode_statistically_equal(config1):
+    """FAST (DDA majorants, ratio-tracked NEE) converges to PARITY: the frame
+    mean agrees to 1.5% and the per-pixel error is at the Monte-Carlo noise
+    floor measured between two independent parity frames."""
     ctx, _, _, _ = config1
     cam = CameraSpec(64, 64)
-    par = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=1, mode="parity"))
-    fast = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=1, mode="fast"))
-    rel = np.sqrt(np.mean((fast - par) ** 2)) / par.mean()
-    print("fast vs parity rel rmse", rel)
-    assert rel < 0.05
+    par = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=1, mode="parity")).astype(np.float64)
+    par2 = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=2, mode="parity")).astype(np.float64)
+    fast = ctx.render_neural(cam, RenderConfig(spp=64, g=0.5, seed=3, mode="fast")).astype(np.float64)
+    noise = np.sqrt(np.mean((par2 - par) ** 2))
+    err = np.sqrt(np.mean((fast - par) ** 2))
+    print("fast vs parity rmse", err, "noise floor", noise, "means", fast.mean(), par.mean())
+    assert abs(fast.mean() - par.mean()) / par.mean() < 0.015
+    assert err < 1.2 * noise
 
 
 @pytest.mark.parametrize("mode", ["parity", "fast"])

@@ -140,3 +140,21 @@ def test_camera_basis(pflib, oracle):
             assert list(getattr(a, f)) == list(getattr(b, f))
     with pytest.raises(ValueError):
         Context.camera(CameraSpec(8, 8, (0, 0, 0), (0, 1, 0), (0, 1, 0)))
+
+
+def test_cpp_shim_against_reference_headers(pflib, tmp_path):
+    """include/pf/gpu.hpp compiles with the reference's headers and links the C ABI."""
+    import shutil
+    import subprocess
+    ref_inc = Path("/root/reference/proj/include")
+    if not ref_inc.exists() or not shutil.which("g++"):
+        pytest.skip("reference headers not present")
+    exe = tmp_path / "shim_smoke"
+    libdir = pflib.LIB_PATH.parent
+    cmd = ["g++", "-std=gnu++20", "-O1", f"-I{ref_inc}", f"-I{ROOT / 'include'}",
+           str(ROOT / "tests" / "cpp" / "shim_smoke.cpp"), "/root/reference/proj/src/volume.cpp",
+           "-o", str(exe), f"-L{libdir}", "-lpfgpu", f"-Wl,-rpath,{libdir}"]
+    subprocess.run(cmd, check=True, capture_output=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert ("no gpu" in r.stdout) or ("gpu ok hits=4" in r.stdout)
