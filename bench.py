@@ -77,7 +77,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.01)
 
     def __enter__(self):
         if self.nv:
@@ -163,7 +163,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
@@ -343,7 +343,7 @@ def main():
                          "peak_source": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 3 * args.steps + (3 * args.steps if world > 1 else 0),
+            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) + (2 * args.steps if world > 1 else 0),
             "clocks": clk.summary(),
             **extras,
         }

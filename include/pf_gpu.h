@@ -50,8 +50,10 @@ extern "C" {
  * PARITY: binary64 delta tracking with the reference's exact operation order
  *   and RNG consumption; NEE transmittance = nee_trials delta-tracked flights
  *   exactly as pf::transmittance (proj/src/volume.cpp:227-256).
- * FAST:   binary32 delta tracking (same streams, 2 x u32 per uniform) and
- *   ratio-tracked shadow rays with Russian roulette; statistically equal. */
+ * FAST:   binary32 delta tracking against per-macro-cell majorants (DDA walk
+ *   over PF_MACRO^3-voxel cells; empty space skipped) and ratio-tracked
+ *   shadow rays with Russian roulette; unbiased, statistically equal to
+ *   PARITY (same per-sample streams, consumed differently). */
 #define PF_MODE_PARITY 0
 #define PF_MODE_FAST 1
 
@@ -106,6 +108,7 @@ typedef struct {
     uint64_t primary_steps;  /* tentative collisions, primary rays */
     uint64_t shadow_steps;   /* tentative collisions, shadow rays */
     float ms_trace, ms_field, ms_compose; /* device time per stage (0 unless timing on) */
+    uint32_t kernel_launches;              /* device kernels this call launched */
 } pf_render_stats;
 
 /* Photon record, pf::Photon (proj/include/pf/photon.hpp:17-22): 40 bytes. */

@@ -47,7 +47,7 @@ class RenderDesc(C.Structure):
 class RenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("hits", C.c_uint64), ("primary_steps", C.c_uint64),
                 ("shadow_steps", C.c_uint64), ("ms_trace", C.c_float), ("ms_field", C.c_float),
-                ("ms_compose", C.c_float)]
+                ("ms_compose", C.c_float), ("kernel_launches", C.c_uint32)]
 
 
 class Photon(C.Structure):

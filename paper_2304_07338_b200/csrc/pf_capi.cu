@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -111,6 +112,13 @@ double tf_classify_alpha(const std::vector<double> &pts, double scalar) {
     return a[4] + (b[4] - a[4]) * t;
 }
 
+// Macro-cell edge in voxels (PF_MACRO; PF_MACRO_CELL overrides it for tuning sweeps).
+int macro_default() {
+    const char *e = std::getenv("PF_MACRO_CELL");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 2 && v <= 64 ? v : PF_MACRO;
+}
+
 }  // namespace
 
 struct pf_ctx {
@@ -124,6 +132,7 @@ struct pf_ctx {
     cudaTextureObject_t vol_tex = 0;
     int atlas_log2 = 0;
     int mc[3] = {0, 0, 0};
+    int macro = macro_default();  // voxels per macro-cell edge
     DevBuf macro_mm, maj, tf_dev;
     int nx = 0, ny = 0, nz = 0;
     float vmin = 0.f, vmax = 0.f;
@@ -136,7 +145,7 @@ struct pf_ctx {
     bool has_field = false;
     FieldDesc fdesc{};
     FieldHost fhost;
-    DevBuf f_tables, f_img;
+    DevBuf f_tables, f_img, f_feat;
     int f_nwg = 0;
     size_t f_smem = 0;
     int sms = 0;
@@ -179,8 +188,8 @@ struct pf_ctx {
         for (int a = 0; a < 3; ++a) {
             const int n = a == 0 ? nx : a == 1 ? ny : nz;
             S.mc[a] = mc[a];
-            S.mh[a] = (float)PF_MACRO / (float)n;
-            S.minv_h[a] = (float)n / (float)PF_MACRO;
+            S.mh[a] = (float)macro / (float)n;
+            S.minv_h[a] = (float)n / (float)macro;
         }
         S.nx = nx;
         S.ny = ny;
@@ -334,12 +343,12 @@ int pf_volume_upload(pf_ctx *c, int nx, int ny, int nz, const float *data) {
     PF_CUDA(cudaMemcpyAsync(lin.p, src, n * 4, cudaMemcpyHostToDevice, c->stream));
     PF_CUDA(launch_build_atlas((const float *)lin.p, nx, ny, nz, lg, (float *)atl.p, aw, ah, c->stream));
     // FAST-mode macro-cell scalar ranges (majorants are derived per TF in pf_medium_set)
-    for (int a = 0; a < 3; ++a) c->mc[a] = ((a == 0 ? nx : a == 1 ? ny : nz) + PF_MACRO - 1) / PF_MACRO;
+    for (int a = 0; a < 3; ++a) c->mc[a] = ((a == 0 ? nx : a == 1 ? ny : nz) + c->macro - 1) / c->macro;
     const size_t ncell = (size_t)c->mc[0] * c->mc[1] * c->mc[2];
     PF_CUDA(c->macro_mm.ensure(ncell * sizeof(float2)));
     PF_CUDA(c->maj.ensure(ncell * sizeof(float)));
     PF_CUDA(launch_macro_minmax((const float *)lin.p, nx, ny, nz, (float2 *)c->macro_mm.p, c->mc[0], c->mc[1],
-                                c->mc[2], c->stream));
+                                c->mc[2], c->macro, c->stream));
     cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
     PF_CUDA(cudaMallocArray(&c->vol_array, &fd, aw, ah));
     PF_CUDA(cudaMemcpy2DToArrayAsync(c->vol_array, 0, 0, atl.p, aw * 4, aw * 4, ah, cudaMemcpyDeviceToDevice,
@@ -505,6 +514,30 @@ int pf_field_load(pf_ctx *c, const pf_field_desc *d, const float *params, size_t
     return PF_OK;
 }
 
+// Feature-tile staging budget (HBM): the hit count is only known on the
+// device, so renders launch ceil(n_work / cap) encode+MLP pairs and the
+// surplus pairs exit immediately.  8 GiB keeps C2 (16.6M samples, paper
+// field: 640 B/row) to two pairs.
+static constexpr size_t kFieldStageBytes = (size_t)8 << 30;
+static constexpr size_t kFieldRowCap = (size_t)1 << 22;
+
+// encode + MLP over n_max items (count on device for renders), in row batches
+static int run_field(pf_ctx *c, FieldParams P, size_t n_max, uint32_t *launches = nullptr) {
+    const size_t row_bytes = (size_t)P.nch * 128u;  // 16 KB per chunk per 128 rows
+    const size_t cap = std::min(n_max, std::max(kFieldRowCap, kFieldStageBytes / row_bytes));
+    PF_CUDA(c->f_feat.ensure(field_feat_bytes(c->fhost, cap)));
+    P.feat = (uint8_t *)c->f_feat.p;
+    P.row_cap = cap;
+    for (size_t r0 = 0; r0 < n_max; r0 += cap) {
+        P.row0 = r0;
+        const size_t tiles = (std::min(cap, n_max - r0) + 127) / 128;
+        const int grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)c->sms, (tiles + P.n_wg - 1) / P.n_wg));
+        PF_CUDA(launch_field(P, c->fhost.fp, c->fhost.fd, grid, c->f_smem, c->stream));
+        if (launches) *launches += 2;
+    }
+    return PF_OK;
+}
+
 static FieldParams field_params(pf_ctx *c) {
     FieldParams P;
     std::memset(&P, 0, sizeof(P));
@@ -523,6 +556,8 @@ static FieldParams field_params(pf_ctx *c) {
     for (size_t i = 0; i < h.levels.size(); ++i) P.lv[i] = h.levels[i];
     P.tables = (const __half *)c->f_tables.p;
     P.img = c->f_img.p;
+    P.nch = (h.K0 + 63) / 64;
+    P.row_cap = kFieldRowCap;
     return P;
 }
 
@@ -547,9 +582,7 @@ int pf_field_query(pf_ctx *c, size_t n, const float *x3, const float *w2, const 
     P.qg = (const float *)dg;
     P.qout = (float *)dout;
     P.decoded = decoded;
-    const size_t tiles = (n + 127) / 128;
-    int grid = (int)std::min<size_t>((size_t)c->sms, (tiles + P.n_wg - 1) / P.n_wg);
-    PF_CUDA(launch_field(P, c->fhost.fp, c->fhost.fd, std::max(grid, 1), c->f_smem, c->stream));
+    if (int e = run_field(c, P, n)) return e;
     if (host_out) {
         PF_CUDA(cudaMemcpyAsync(out, dout, n * 12, cudaMemcpyDeviceToHost, c->stream));
         PF_CUDA(cudaStreamSynchronize(c->stream));
@@ -688,8 +721,10 @@ int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, f
     P.counters = (unsigned long long *)c->counters.p;
     const DevScene S = c->scene();
 
+    uint32_t n_launch = 0;
     if (c->timing) cudaEventRecord(c->ev[0], c->stream);
     if (n_work) {
+        ++n_launch;
         const int grid = parity ? trace_grid_size_parity(c->device) : trace_grid_size_fast(c->device);
         PF_CUDA(parity ? launch_render_trace_parity(S, P, grid, c->stream)
                        : launch_render_trace_fast(S, P, grid, c->stream));
@@ -704,12 +739,13 @@ int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, f
         F.slot_f64 = parity ? 1 : 0;
         F.w_i = d->w_i;
         F.g_render = (float)d->g;
-        PF_CUDA(launch_field(F, c->fhost.fp, c->fhost.fd, c->sms, c->f_smem, c->stream));
+        if (int e = run_field(c, F, n_work, &n_launch)) return e;
     }
     if (c->timing) cudaEventRecord(c->ev[2], c->stream);
     C.slots = c->slots.p;
     C.out = (float *)frame;
     PF_CUDA(launch_compose(parity, C, c->stream));
+    if (C.n_local_tiles) ++n_launch;
     if (c->timing) cudaEventRecord(c->ev[3], c->stream);
     if (host_out)
         PF_CUDA(cudaMemcpyAsync(out_rgb, frame, (size_t)cam->width * cam->height * 12, cudaMemcpyDeviceToHost,
@@ -737,6 +773,7 @@ int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, f
             }
         }
         stats->samples = samples;
+        stats->kernel_launches = n_launch;
         if (c->timing) {
             cudaEventElapsedTime(&stats->ms_trace, c->ev[0], c->ev[1]);
             cudaEventElapsedTime(&stats->ms_field, c->ev[1], c->ev[2]);

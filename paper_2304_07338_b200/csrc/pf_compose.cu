@@ -103,13 +103,14 @@ cudaError_t launch_build_atlas(const float *vol, int nx, int ny, int nz, int lg,
 
 // Per macro cell: min/max scalar over the voxels a trilinear sample inside
 // the cell can touch (indices [c*B-1, c*B+B], clamped).
-__global__ void k_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy, int mcz) {
+__global__ void k_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy, int mcz,
+                               int B) {
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= (size_t)mcx * mcy * mcz) return;
     const int cx = (int)(c % mcx), cy = (int)((c / mcx) % mcy), cz = (int)(c / ((size_t)mcx * mcy));
-    const int x0 = max(cx * PF_MACRO - 1, 0), x1 = min(cx * PF_MACRO + PF_MACRO, nx - 1);
-    const int y0 = max(cy * PF_MACRO - 1, 0), y1 = min(cy * PF_MACRO + PF_MACRO, ny - 1);
-    const int z0 = max(cz * PF_MACRO - 1, 0), z1 = min(cz * PF_MACRO + PF_MACRO, nz - 1);
+    const int x0 = max(cx * B - 1, 0), x1 = min(cx * B + B, nx - 1);
+    const int y0 = max(cy * B - 1, 0), y1 = min(cy * B + B, ny - 1);
+    const int z0 = max(cz * B - 1, 0), z1 = min(cz * B + B, nz - 1);
     float lo = 1e30f, hi = -1e30f;
     for (int z = z0; z <= z1; ++z)
         for (int y = y0; y <= y1; ++y)
@@ -142,9 +143,9 @@ __global__ void k_macro_majorant(const float2 *mm, size_t ncells, const double *
 }
 
 cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy, int mcz,
-                                cudaStream_t st) {
+                                int B, cudaStream_t st) {
     const size_t n = (size_t)mcx * mcy * mcz;
-    k_macro_minmax<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(vol, nx, ny, nz, mm, mcx, mcy, mcz);
+    k_macro_minmax<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(vol, nx, ny, nz, mm, mcx, mcy, mcz, B);
     return cudaGetLastError();
 }
 

@@ -30,115 +30,109 @@ namespace pfk {
 
 constexpr uint32_t kPrime1 = 2654435761u, kPrime2 = 805459861u;
 
-__device__ __forceinline__ void load_feats(const __half *tab, uint32_t e, float *v, int F) {
-    if (F == 8) {
-        uint4 u = __ldg(reinterpret_cast<const uint4 *>(tab) + e);
-        const __half2 *h = reinterpret_cast<const __half2 *>(&u);
+template <int F>
+struct Raw;  // one table entry (F fp16 features)
+template <>
+struct Raw<8> {
+    uint4 v;
+};
+template <>
+struct Raw<4> {
+    uint2 v;
+};
+template <>
+struct Raw<2> {
+    uint32_t v;
+};
+
+template <int F>
+__device__ __forceinline__ Raw<F> load_raw(const __half *tab, uint32_t e) {
+    Raw<F> r;
+    if constexpr (F == 8) r.v = __ldg(reinterpret_cast<const uint4 *>(tab) + e);
+    else if constexpr (F == 4) r.v = __ldg(reinterpret_cast<const uint2 *>(tab) + e);
+    else r.v = __ldg(reinterpret_cast<const uint32_t *>(tab) + e);
+    return r;
+}
+
+template <int F>
+__device__ __forceinline__ void accum_raw(const Raw<F> &r, float w, float *acc) {
+    const __half2 *h = reinterpret_cast<const __half2 *>(&r.v);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            float2 f = __half22float2(h[i]);
-            v[2 * i] = f.x;
-            v[2 * i + 1] = f.y;
-        }
-    } else if (F == 4) {
-        uint2 u = __ldg(reinterpret_cast<const uint2 *>(tab) + e);
-        const __half2 *h = reinterpret_cast<const __half2 *>(&u);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            float2 f = __half22float2(h[i]);
-            v[2 * i] = f.x;
-            v[2 * i + 1] = f.y;
-        }
-    } else {
-        uint32_t u = __ldg(reinterpret_cast<const uint32_t *>(tab) + e);
-        float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&u));
-        v[0] = f.x;
-        v[1] = f.y;
+    for (int i = 0; i < F / 2; ++i) {
+        const float2 f = __half22float2(h[i]);
+        acc[2 * i] = fmaf(w, f.x, acc[2 * i]);
+        acc[2 * i + 1] = fmaf(w, f.y, acc[2 * i + 1]);
     }
 }
 
-__device__ __forceinline__ void store_feats(uint8_t *A, int r, int k, uint32_t sbo, const float *acc,
-                                            int F) {
-    uint8_t *p = A + (r >> 3) * sbo + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
-    if (F == 8) {
-        uint4 u;
-        __half2 *h = reinterpret_cast<__half2 *>(&u);
+// st.shared of F fp16 features of row r at column k of an UMMA tile.
+template <int F>
+__device__ __forceinline__ void store_feats(uint32_t A_s, int r, int k, uint32_t sbo, const float *acc) {
+    const uint32_t a = A_s + (uint32_t)(r >> 3) * sbo + (uint32_t)(k >> 3) * 128u + (uint32_t)(r & 7) * 16u +
+                       (uint32_t)(k & 7) * 2u;
+    uint32_t h[F / 2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(acc[2 * i], acc[2 * i + 1]);
-        *reinterpret_cast<uint4 *>(p) = u;
-    } else if (F == 4) {
-        uint2 u;
-        __half2 *h = reinterpret_cast<__half2 *>(&u);
-        h[0] = __floats2half2_rn(acc[0], acc[1]);
-        h[1] = __floats2half2_rn(acc[2], acc[3]);
-        *reinterpret_cast<uint2 *>(p) = u;
-    } else {
-        __half2 h = __floats2half2_rn(acc[0], acc[1]);
-        *reinterpret_cast<__half2 *>(p) = h;
+    for (int i = 0; i < F / 2; ++i) {
+        __half2 v = __floats2half2_rn(acc[2 * i], acc[2 * i + 1]);
+        h[i] = *reinterpret_cast<uint32_t *>(&v);
+    }
+    if constexpr (F == 8)
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]));
+    else if constexpr (F == 4)
+        asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(a), "r"(h[0]), "r"(h[1]));
+    else
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(h[0]));
+}
+
+__device__ __forceinline__ void st_shared_zero16(uint32_t a) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(0u));
+}
+
+// Cell + fractional weights of one level (exact p*N split: s + e == p*N).
+template <int D>
+__device__ __forceinline__ void level_cell(const FieldLevel &L, const float *pin, uint32_t *c, float *f) {
+    const float resf = (float)L.res;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const float s = pin[i] * resf;
+        const float e = fmaf(pin[i], resf, -s);
+        const float fl = floorf(s);
+        float fr = (s - fl) + e;
+        int ci = (int)fl;
+        if (fr < 0.f) {
+            ci -= 1;
+            fr += 1.f;
+        }
+        if (ci > (int)L.res - 1) {
+            ci = (int)L.res - 1;
+            fr = (s - (float)ci) + e;
+        }
+        c[i] = (uint32_t)ci;
+        f[i] = fr;
     }
 }
 
-// Multilinear hash-grid encoding of one D-dim input into A row r, columns
-// [kbase, kbase + levels*F) (pinned in oracle or_hashgrid_encode).
-template <int D, int F>
-__device__ __forceinline__ void encode_grid(const FieldParams &P, int lv0, int nlv, const float *in,
-                                            uint8_t *A, int r, int kbase, uint32_t sbo) {
-    float pin[D];
+template <int D>
+__device__ __forceinline__ uint32_t corner_index(const FieldLevel &L, const uint32_t *c, int corner) {
+    uint32_t v[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) pin[i] = __saturatef(in[i]);
-    for (int l = 0; l < nlv; ++l) {
-        const FieldLevel L = P.lv[lv0 + l];
-        const float resf = (float)L.res;
-        uint32_t c[D];
-        float f[D];
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-            // exact p*N split: s + e == p*N, so the cell fraction keeps full precision
-            const float s = pin[i] * resf;
-            const float e = fmaf(pin[i], resf, -s);
-            float fl = floorf(s);
-            float fr = (s - fl) + e;
-            int ci = (int)fl;
-            if (fr < 0.f) {
-                ci -= 1;
-                fr += 1.f;
-            }
-            if (ci > (int)L.res - 1) {
-                ci = (int)L.res - 1;
-                fr = (s - (float)ci) + e;
-            }
-            c[i] = (uint32_t)ci;
-            f[i] = fr;
-        }
-        float acc[F];
-#pragma unroll
-        for (int k = 0; k < F; ++k) acc[k] = 0.f;
-#pragma unroll
-        for (int corner = 0; corner < (1 << D); ++corner) {
-            float w = 1.f;
-            uint32_t v[D];
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-                const int bit = (corner >> i) & 1;
-                w *= bit ? f[i] : (1.f - f[i]);
-                v[i] = c[i] + (uint32_t)bit;
-            }
-            uint32_t idx;
-            if (L.dense) {
-                idx = v[0] + L.n1 * v[1];
-                if (D == 3) idx += L.n1 * L.n1 * v[D - 1];
-            } else {
-                uint32_t h = v[0] ^ (v[1] * kPrime1);
-                if (D == 3) h ^= v[D - 1] * kPrime2;
-                idx = h & L.mask;
-            }
-            float e[F];
-            load_feats(P.tables + L.offset_halves, idx, e, F);
-#pragma unroll
-            for (int k = 0; k < F; ++k) acc[k] = fmaf(w, e[k], acc[k]);
-        }
-        store_feats(A, r, kbase + l * F, sbo, acc, F);
+    for (int i = 0; i < D; ++i) v[i] = c[i] + (uint32_t)((corner >> i) & 1);
+    if (L.dense) {
+        uint32_t idx = v[0] + L.n1 * v[1];
+        if (D == 3) idx += L.n1 * L.n1 * v[D - 1];
+        return idx;
     }
+    uint32_t h = v[0] ^ (v[1] * kPrime1);
+    if (D == 3) h ^= v[D - 1] * kPrime2;
+    return h & L.mask;
+}
+
+template <int D>
+__device__ __forceinline__ float corner_weight(const float *f, int corner) {
+    float w = 1.f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) w *= ((corner >> i) & 1) ? f[i] : (1.f - f[i]);
+    return w;
 }
 
 __device__ __forceinline__ void issue_layer(uint32_t a_s, uint32_t b_s, int K, int N, uint32_t tmem_d) {
@@ -151,24 +145,120 @@ __device__ __forceinline__ void issue_layer(uint32_t a_s, uint32_t b_s, int K, i
     }
 }
 
-// Zero-pad columns [k0, k1) of row r in a chunk tile of width W (multiples of 8).
-__device__ __forceinline__ void zero_cols(uint8_t *A, int r, int k0, int k1, uint32_t sbo) {
-    for (int k = k0; k < k1; k += 8)
-        *reinterpret_cast<uint4 *>(A + (r >> 3) * sbo + (k >> 3) * 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+// Encode ONE level of one input (pinned in oracle
+// or_hashgrid_encode): 2^D gathers issued back to back, fp32 accumulation.
+template <int D, int F>
+__device__ __forceinline__ void encode_level(const FieldParams &P, int lv, const float *pin, float *acc) {
+    constexpr int NC = 1 << D;
+    const FieldLevel L = P.lv[lv];
+    uint32_t c[D];
+    float f[D];
+    level_cell<D>(L, pin, c, f);
+    Raw<F> e[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) e[k] = load_raw<F>(P.tables + L.offset_halves, corner_index<D>(L, c, k));
+#pragma unroll
+    for (int k = 0; k < F; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) accum_raw<F>(e[k], corner_weight<D>(f, k), acc);
 }
 
+// Byte offset of element (row, k) in the feature-tile buffer: tile-major,
+// then 64-column chunks of 16 KB, each a canonical K-major UMMA tile.
+__device__ __forceinline__ size_t feat_off(const FieldParams &P, size_t row, int k) {
+    const size_t tile = row >> 7;
+    const int r = (int)(row & 127), chunk = k >> 6, kk = k & 63;
+    const int kw = min(64, P.K0 - 64 * chunk);
+    return (tile * (size_t)P.nch + (size_t)chunk) * 16384u + (size_t)((r >> 3) * kw * 16 + (kk >> 3) * 128 +
+                                                                     (r & 7) * 16 + (kk & 7) * 2);
+}
+
+template <int F>
+__device__ __forceinline__ void st_feats_global(uint8_t *p, const float *acc) {
+    uint32_t h[F / 2];
+#pragma unroll
+    for (int i = 0; i < F / 2; ++i) {
+        __half2 v = __floats2half2_rn(acc[2 * i], acc[2 * i + 1]);
+        h[i] = *reinterpret_cast<uint32_t *>(&v);
+    }
+    if constexpr (F == 8) *reinterpret_cast<uint4 *>(p) = make_uint4(h[0], h[1], h[2], h[3]);
+    else if constexpr (F == 4) *reinterpret_cast<uint2 *>(p) = make_uint2(h[0], h[1]);
+    else *reinterpret_cast<uint32_t *>(p) = h[0];
+}
+
+// K3: hash-grid encoding, one thread per (query, unit); a warp covers 8
+// queries x 4 units so each level's 8 rows land as one contiguous 128-byte
+// store.  Units: pos levels, dir levels, then one "g + zero padding" unit.
 template <int FP, int FD>
-__global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
+__global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
+    const size_t n_all = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
+    const size_t n = n_all > P.row0 ? min(n_all - P.row0, P.row_cap) : 0;  // rows of this launch
+    const size_t n_rows = (n + 127) & ~(size_t)127;  // whole tiles (pad rows encode zeros)
+    const int U = P.n_pos_levels + P.n_dir_levels + 1, U4 = (U + 3) >> 2;
+    const size_t n_wu = (n_rows >> 3) * (size_t)U4;
+    const int lane = threadIdx.x & 31;
+    const size_t warp0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const size_t n_warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t wu = warp0; wu < n_wu; wu += n_warps) {
+        const size_t row = (wu / U4) * 8 + (lane & 7);
+        const int u = (int)(wu % U4) * 4 + (lane >> 3);
+        if (u >= U) continue;
+        const bool valid = row < n;
+        const size_t gr = P.row0 + row;  // global item index
+        float x[3] = {0.f, 0.f, 0.f}, ws[2] = {0.f, 0.f}, gin = 0.f;
+        if (valid) {
+            if (P.mode == 0) {
+                const HitRec h = P.hits[gr];
+                x[0] = h.x[0], x[1] = h.x[1], x[2] = h.x[2];
+                ws[0] = h.wsph[0], ws[1] = h.wsph[1];
+                gin = P.g_render;
+            } else {
+                x[0] = P.qx[3 * gr], x[1] = P.qx[3 * gr + 1], x[2] = P.qx[3 * gr + 2];
+                ws[0] = P.qw[2 * gr], ws[1] = P.qw[2 * gr + 1];
+                gin = P.qg[gr];
+            }
+        }
+        if (u < P.n_pos_levels) {
+            float pin[3] = {__saturatef(x[0]), __saturatef(x[1]), __saturatef(x[2])};
+            float acc[FP];
+            encode_level<3, FP>(P, u, pin, acc);
+            st_feats_global<FP>(P.feat + feat_off(P, row, u * FP), acc);
+        } else if (u < P.n_pos_levels + P.n_dir_levels) {
+            const int l = u - P.n_pos_levels;
+            float pin[2] = {__saturatef(ws[0]), __saturatef(ws[1])};
+            float acc[FD];
+            encode_level<2, FD>(P, P.n_pos_levels + l, pin, acc);
+            st_feats_global<FD>(P.feat + feat_off(P, row, P.n_pos_levels * FP + l * FD), acc);
+        } else {
+            const int kg = P.n_pos_levels * FP + P.n_dir_levels * FD;  // multiple of 8
+            const uint32_t gh = valid ? (uint32_t)__half_as_ushort(__float2half_rn((gin + 1.0f) * 0.5f)) : 0u;
+            *reinterpret_cast<uint4 *>(P.feat + feat_off(P, row, kg)) = make_uint4(gh, 0u, 0u, 0u);
+            for (int k = kg + 8; k < P.K0; k += 8)
+                *reinterpret_cast<uint4 *>(P.feat + feat_off(P, row, k)) = make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
+}
+
+// K4: the MLP on tcgen05.  Persistent CTA per SM with the whole MLP image in
+// shared memory; each warpgroup owns a 128-row tile pipeline:
+//   layer 0: chunk j of the feature tile arrives by ONE 1-D bulk TMA copy
+//            (double-buffered, mbarrier complete_tx) and is consumed by
+//            kw/16 tcgen05.mma (M=128, N=64, K=16) into a 64-column TMEM
+//            accumulator while chunk j+1 is in flight;
+//   layers 1..H: tcgen05.ld -> bias + ReLU -> fp16 -> st.shared into the A
+//            tile -> next layer's MMA (N=16 for the 3-wide output layer);
+//   epilogue: Eq. 8 decode, compose term into the sample's slot.
+__global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *img = smem;
     uint8_t *abase = smem + P.img_bytes;
-    // per warpgroup: two 128 x 64 fp16 chunk tiles (16 KB each) + 2 mbarriers
+    // barriers: [0] weights; per warpgroup w: 1+5w: full0, full1, empty0, empty1, done
     uint64_t *bars = reinterpret_cast<uint64_t *>(abase + (size_t)P.n_wg * 32768);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + 2 * P.n_wg);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + 5 * P.n_wg);
 
     const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5;
     if (tid == 0) {
-        for (int i = 0; i <= 2 * P.n_wg; ++i) mbar_init(smem_u32(&bars[i]), 1);
+        for (int i = 0; i <= 5 * P.n_wg; ++i) mbar_init(smem_u32(&bars[i]), 1);
         mbar_fence_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), P.tmem_cols);
@@ -182,119 +272,83 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
     const uint32_t tmem_base = *tmem_slot;
     mbar_wait(smem_u32(&bars[0]), 0);
 
-    const size_t n_items = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
+    const size_t n_all = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
+    const size_t n_items = n_all > P.row0 ? min(n_all - P.row0, P.row_cap) : 0;
     const size_t n_tiles = (n_items + 127) / 128;
-    uint8_t *buf[2] = {abase + (size_t)wg * 32768, abase + (size_t)wg * 32768 + 16384};
-    const uint32_t buf_s[2] = {smem_u32(buf[0]), smem_u32(buf[1])};
+    const uint32_t buf_s[2] = {smem_u32(abase + (size_t)wg * 32768), smem_u32(abase + (size_t)wg * 32768 + 16384)};
     const uint32_t img_s = smem_u32(img);
     const uint32_t tmem_wg = tmem_base + (uint32_t)(wg * 64);
     const uint32_t tmem_rows = tmem_wg + ((uint32_t)(32 * (warp & 3)) << 16);
-    const uint32_t mbar[2] = {smem_u32(&bars[1 + 2 * wg]), smem_u32(&bars[2 + 2 * wg])};
-    uint32_t ph[2] = {0u, 0u};
-    bool pending[2] = {false, false};
+    uint64_t *wb = bars + 1 + 5 * wg;
+    const uint32_t full[2] = {smem_u32(&wb[0]), smem_u32(&wb[1])};
+    const uint32_t empty[2] = {smem_u32(&wb[2]), smem_u32(&wb[3])};
+    const uint32_t done = smem_u32(&wb[4]);
+    uint32_t ph_full[2] = {0u, 0u}, ph_empty[2] = {0u, 0u}, ph_done = 0u;
+    bool empty_pending[2] = {false, false};
     const float *bias = reinterpret_cast<const float *>(img + P.off_bias);
-    const int kdir = P.n_pos_levels * FP;
-    const int kg = kdir + P.n_dir_levels * FD;     // column of the g input
-    const int nch = (P.K0 + 63) / 64;
     const uint32_t sbo_w0 = (uint32_t)P.K0 * 16u;
 
-    auto wait_buf = [&](int b) {
-        if (pending[b]) {
-            mbar_wait(mbar[b], ph[b]);
-            ph[b] ^= 1u;
-            pending[b] = false;
-        }
-    };
-
     for (size_t tile = (size_t)blockIdx.x * P.n_wg + wg; tile < n_tiles; tile += (size_t)gridDim.x * P.n_wg) {
-        const size_t row = tile * 128 + r;
-        const bool valid = row < n_items;
-        float x[3] = {0.f, 0.f, 0.f}, ws[2] = {0.f, 0.f}, gin = 0.f;
-        uint32_t slot = 0;
-        double sigma_s = 0.0;
-        if (valid) {
-            if (P.mode == 0) {
-                const HitRec h = P.hits[row];
-                x[0] = h.x[0];
-                x[1] = h.x[1];
-                x[2] = h.x[2];
-                ws[0] = h.wsph[0];
-                ws[1] = h.wsph[1];
-                slot = h.slot;
-                sigma_s = h.sigma_s;
-                gin = P.g_render;
-            } else {
-                x[0] = P.qx[3 * row];
-                x[1] = P.qx[3 * row + 1];
-                x[2] = P.qx[3 * row + 2];
-                ws[0] = P.qw[2 * row];
-                ws[1] = P.qw[2 * row + 1];
-                gin = P.qg[row];
-            }
-        }
-        // ---- K3 + layer-0 MMA, chunk by chunk (encode j+1 overlaps MMA j)
-        for (int j = 0; j < nch; ++j) {
-            const int b = j & 1;
-            const int k0 = 64 * j, kw = min(64, P.K0 - k0);
-            const uint32_t sbo = (uint32_t)kw * 16u;
-            wait_buf(b);  // the MMA that last read this buffer is done
-            uint8_t *A = buf[b];
-            // position levels whose features start in [k0, k0+kw)
-            const int lp0 = min(P.n_pos_levels, k0 / FP), lp1 = min(P.n_pos_levels, (k0 + kw) / FP);
-            if (lp1 > lp0) encode_grid<3, FP>(P, lp0, lp1 - lp0, x, A, r, lp0 * FP - k0, sbo);
-            const int ld0 = min(P.n_dir_levels, max(0, (k0 - kdir + FD - 1) / FD));
-            const int ld1 = min(P.n_dir_levels, max(0, (k0 + kw - kdir + FD - 1) / FD));
-            if (ld1 > ld0) encode_grid<2, FD>(P, P.n_pos_levels + ld0, ld1 - ld0, ws, A, r, kdir + ld0 * FD - k0, sbo);
-            if (kg >= k0 && kg < k0 + kw) {
-                const int kk = kg - k0;
-                uint8_t *p = A + (r >> 3) * sbo + (kk >> 3) * 128 + (r & 7) * 16;
-                uint4 u = make_uint4(0u, 0u, 0u, 0u);
-                u.x = (uint32_t)__half_as_ushort(__float2half_rn((gin + 1.0f) * 0.5f));
-                *reinterpret_cast<uint4 *>(p) = u;
-                zero_cols(A, r, kk + 8, kw, sbo);
-            } else if (kg < k0) {
-                zero_cols(A, r, 0, kw, sbo);
-            }
-            fence_proxy_async_smem();
-            named_bar_sync(1 + wg, 128);
-            if (r == 0) {
+        const uint8_t *tsrc = P.feat + tile * (size_t)P.nch * 16384u;
+        // ---- layer 0: TMA-fed chunks (only thread r == 0 drives the pipeline)
+        if (r == 0) {
+            auto load = [&](int j) {
+                const int b = j & 1;
+                if (empty_pending[b]) {
+                    mbar_wait(empty[b], ph_empty[b]);
+                    ph_empty[b] ^= 1u;
+                    empty_pending[b] = false;
+                }
+                const uint32_t bytes = (uint32_t)min(64, P.K0 - 64 * j) * 256u;  // 128 rows x kw x 2 B
+                mbar_expect_tx(full[b], bytes);
+                bulk_g2s(buf_s[b], tsrc + (size_t)j * 16384u, bytes, full[b]);
+            };
+            load(0);
+            for (int j = 0; j < P.nch; ++j) {
+                const int b = j & 1;
+                if (j + 1 < P.nch) load(j + 1);
+                mbar_wait(full[b], ph_full[b]);
+                ph_full[b] ^= 1u;
                 tc_fence_after();
-                const uint32_t idesc = umma_idesc_f16(128, 64);
+                const int kw = min(64, P.K0 - 64 * j);
+                const uint32_t sbo = (uint32_t)kw * 16u, idesc = umma_idesc_f16(128, 64);
                 for (int s = 0; s < kw / 16; ++s) {
                     const uint64_t ad = umma_sdesc(buf_s[b] + 256u * s, 128u, sbo);
-                    const uint64_t bd = umma_sdesc(img_s + P.off_w[0] + (uint32_t)(k0 / 8) * 128u + 256u * s, 128u,
-                                                   sbo_w0);
+                    const uint64_t bd = umma_sdesc(img_s + P.off_w[0] + (uint32_t)(j * 8) * 128u + 256u * s, 128u, sbo_w0);
                     umma_f16(tmem_wg, ad, bd, idesc, (j > 0 || s > 0) ? 1u : 0u);
                 }
-                umma_commit(mbar[b]);
+                umma_commit(empty[b]);
+                empty_pending[b] = true;
             }
-            pending[b] = true;
+            umma_commit(done);
         }
-        wait_buf(0);
-        wait_buf(1);
+        mbar_wait(done, ph_done);
+        ph_done ^= 1u;
         tc_fence_after();
+        if (r == 0) {  // keep the per-buffer parities in step (both are complete by now)
+            for (int b = 0; b < 2; ++b)
+                if (empty_pending[b]) {
+                    mbar_wait(empty[b], ph_empty[b]);
+                    ph_empty[b] ^= 1u;
+                    empty_pending[b] = false;
+                }
+        }
 
-        // ---- K4: hidden layers (epilogue of layer L-1 feeds the MMA of layer L)
+        // ---- hidden layers (epilogue of layer L-1 feeds the MMA of layer L)
         for (int L = 1; L <= P.hidden_layers; ++L) {
             const int b = L & 1;
-            uint8_t *A = buf[b];
             const float *bl = bias + (L - 1) * 64;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 float v[16];
                 tmem_ld16(tmem_rows + 16 * c, v);
                 tmem_ld_wait();
-                uint4 u[2];
-                __half2 *h = reinterpret_cast<__half2 *>(u);
+                float a[16];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float a0 = fmaxf(v[2 * i] + bl[16 * c + 2 * i], 0.f);
-                    const float a1 = fmaxf(v[2 * i + 1] + bl[16 * c + 2 * i + 1], 0.f);
-                    h[i] = __floats2half2_rn(a0, a1);
-                }
-                uint8_t *p = A + (r >> 3) * 1024 + (2 * c) * 128 + (r & 7) * 16;  // K = 64: SBO = 1024
-                *reinterpret_cast<uint4 *>(p) = u[0];
-                *reinterpret_cast<uint4 *>(p + 128) = u[1];
+                for (int i = 0; i < 16; ++i) a[i] = fmaxf(v[i] + bl[16 * c + i], 0.f);
+                const uint32_t pa = buf_s[b] + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u;  // K=64: SBO 1024
+                store_feats<8>(pa, 0, 16 * c, 1024u, a);
+                store_feats<8>(pa, 0, 16 * c + 8, 1024u, a + 8);
             }
             tc_fence_before();
             fence_proxy_async_smem();
@@ -302,10 +356,10 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
             if (r == 0) {
                 tc_fence_after();
                 issue_layer(buf_s[b], img_s + P.off_w[L], 64, L < P.hidden_layers ? 64 : 16, tmem_wg);
-                umma_commit(mbar[b]);
+                umma_commit(done);
             }
-            pending[b] = true;
-            wait_buf(b);
+            mbar_wait(done, ph_done);
+            ph_done ^= 1u;
             tc_fence_after();
         }
 
@@ -314,25 +368,28 @@ __global__ void __launch_bounds__(512, 1) k_field(const FieldParams P) {
         tmem_ld16(tmem_rows, v);
         tmem_ld_wait();
         tc_fence_before();
-        const float *bo = bias + P.hidden_layers * 64;
-        float o3[3] = {v[0] + bo[0], v[1] + bo[1], v[2] + bo[2]};
-        if (valid) {
+        named_bar_sync(1 + wg, 128);  // all rows read TMEM / A before the next tile reuses them
+        const size_t row = tile * 128 + r, gr = P.row0 + row;
+        if (row < n_items) {
+            const float *bo = bias + P.hidden_layers * 64;
+            const float o3[3] = {v[0] + bo[0], v[1] + bo[1], v[2] + bo[2]};
             if (P.mode == 0) {
+                const HitRec h = P.hits[gr];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const float Li = exp2f(-__saturatef(o3[c]) * P.psi_log2_10);  // Eq. 8
                     if (P.slot_f64) {
-                        double *sp = reinterpret_cast<double *>(P.slots) + 3 * (size_t)slot + c;
-                        *sp = *sp + P.w_i * (sigma_s * (double)Li);
+                        double *sp = reinterpret_cast<double *>(P.slots) + 3 * (size_t)h.slot + c;
+                        *sp = *sp + P.w_i * (h.sigma_s * (double)Li);
                     } else {
-                        float *sp = reinterpret_cast<float *>(P.slots) + 3 * (size_t)slot + c;
-                        *sp = *sp + (float)P.w_i * ((float)sigma_s * Li);
+                        float *sp = reinterpret_cast<float *>(P.slots) + 3 * (size_t)h.slot + c;
+                        *sp = *sp + (float)P.w_i * ((float)h.sigma_s * Li);
                     }
                 }
             } else {
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
-                    P.qout[3 * row + c] = P.decoded ? exp2f(-__saturatef(o3[c]) * P.psi_log2_10) : o3[c];
+                    P.qout[3 * gr + c] = P.decoded ? exp2f(-__saturatef(o3[c]) * P.psi_log2_10) : o3[c];
             }
         }
     }
@@ -483,19 +540,25 @@ int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, int device)
     return n_wg > 0 ? 0 : 1;
 }
 
+size_t field_feat_bytes(const FieldHost &h, size_t n_items) {
+    const size_t nch = (size_t)((h.K0 + 63) / 64);
+    return ((n_items + 127) / 128) * nch * 16384u;
+}
+
 template <int FP, int FD>
-static cudaError_t launch_t(const FieldParams &P, int grid, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_field<FP, FD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    k_field<FP, FD><<<grid, P.n_wg * 128, smem, st>>>(P);
+static cudaError_t launch_encode(const FieldParams &P, int grid, cudaStream_t st) {
+    k_field_encode<FP, FD><<<grid, 256, 0, st>>>(P);
     return cudaGetLastError();
 }
 
-cudaError_t launch_field(const FieldParams &P, int fp, int fd, int grid, size_t smem,
-                         cudaStream_t st) {
+cudaError_t launch_field(const FieldParams &P, int fp, int fd, int grid, size_t smem, cudaStream_t st) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int egrid = sms * 8;  // 2048 resident threads per SM
+    cudaError_t e = cudaErrorInvalidValue;
 #define PF_FIELD_CASE(a, b) \
-    if (fp == a && fd == b) return launch_t<a, b>(P, grid, smem, st);
+    if (fp == a && fd == b) e = launch_encode<a, b>(P, egrid, st);
     PF_FIELD_CASE(2, 2)
     PF_FIELD_CASE(2, 4)
     PF_FIELD_CASE(2, 8)
@@ -506,7 +569,11 @@ cudaError_t launch_field(const FieldParams &P, int fp, int fd, int grid, size_t 
     PF_FIELD_CASE(8, 4)
     PF_FIELD_CASE(8, 8)
 #undef PF_FIELD_CASE
-    return cudaErrorInvalidValue;
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_field_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_field_mlp<<<grid, P.n_wg * 128, smem, st>>>(P);
+    return cudaGetLastError();
 }
 
 }  // namespace pfk

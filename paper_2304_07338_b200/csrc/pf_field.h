@@ -54,6 +54,10 @@ struct FieldParams {
     const float *qx, *qw, *qg;
     float *qout;
     int decoded;
+    // split path: encode kernel -> feature tiles -> TMA-fed MLP kernel
+    uint8_t *feat;     // [tile][chunk][16 KB], UMMA canonical K-major fp16
+    int nch;           // 64-column chunks per tile (last one may be narrower)
+    size_t row0, row_cap;  // this launch handles items [row0, row0 + row_cap)
 };
 
 struct FieldHost {
@@ -71,7 +75,9 @@ size_t field_param_count(const FieldDesc &d);
 const char *field_validate(const FieldDesc &d);
 void field_pack(const FieldDesc &d, const float *params, FieldHost &out);
 int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, int device);
+// encode (grid-stride, full occupancy) + MLP (persistent, n_wg warpgroups)
 cudaError_t launch_field(const FieldParams &P, int fp, int fd, int grid, size_t smem,
                          cudaStream_t st);
+size_t field_feat_bytes(const FieldHost &h, size_t n_items);
 
 }  // namespace pfk

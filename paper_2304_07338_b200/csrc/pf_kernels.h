@@ -5,7 +5,7 @@
 #include <stdint.h>
 
 #define PF_TRACE_THREADS 128
-#define PF_MACRO 8  // voxels per macro-cell edge (FAST-mode majorant grid)
+#define PF_MACRO 8  // default voxels per macro-cell edge (FAST-mode majorant grid)
 
 namespace pfk {
 
@@ -92,7 +92,7 @@ cudaError_t launch_tiles_unpack(const ComposeParams &C, const float *packed_all,
                                 size_t per_shard_floats, float *frame, cudaStream_t st);
 int trace_grid_size(bool parity, int device);
 cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy,
-                                int mcz, cudaStream_t st);
+                                int mcz, int macro, cudaStream_t st);
 cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const double *tf_pts, int n_tf,
                                   double density_scale, float *maj, cudaStream_t st);
 cudaError_t launch_build_atlas(const float *vol, int nx, int ny, int nz, int log2_cols, float *atlas,

@@ -78,6 +78,22 @@ __device__ __forceinline__ float rsqrt_len(float v) { return sqrtf(v); }
 __device__ __forceinline__ double rinf(double) { return __longlong_as_double(0x7ff0000000000000ll); }
 __device__ __forceinline__ float rinf(float) { return __int_as_float(0x7f800000); }
 
+// Conservative bound on sigma(x) from the macro-cell majorant grid: every
+// trilinear sample inside the cell is covered (cell support +-1 voxel), so
+// u2 * sigma_max >= bound implies the reference rejects the tentative
+// collision (volume.cpp:222-223).  Used to skip the fetch + classify of
+// certain null collisions WITHOUT changing the RNG sequence or any decision.
+__device__ __forceinline__ double cell_bound(const DevScene &S, const double x[3]) {
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        // fmax/fmin also map NaN to a valid cell (the bound is then just looser)
+        const double p = fmin(fmax(x[a] * (double)S.minv_h[a], 0.0), (double)(S.mc[a] - 1));
+        c[a] = (int)p;
+    }
+    return (double)__ldg(S.maj + c[0] + S.mc[0] * (c[1] + S.mc[1] * c[2]));
+}
+
 // One light's NEE term (pinned: oracle/pf_oracle.c or_nee_term).
 template <typename R>
 __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3], const R wo[3], R g,
@@ -170,10 +186,14 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS)
             flight_done = true;
         } else {
             R x[3] = {o[0] + d[0] * t, o[1] + d[1] * t, o[2] + d[2] * t};
+            // u2 is drawn before sigma(x) is evaluated: nothing else touches the
+            // stream in between, so the sequence is the reference's
+            const R u2 = uniform(rng, R(0));
+            if (u2 * sm >= (R)cell_bound(S, x)) continue;  // certain null collision
             const R scalar = sample(S, x);
             const R sigma = ds * tf_alpha(S, scalar);
             if (phase == 1) {
-                if (uniform(rng, R(0)) * sm < sigma) {
+                if (u2 * sm < sigma) {
                     // real interaction: Interaction{x, scalar, albedo}
                     tf_rgba(S, scalar, rgba);
 #pragma unroll
@@ -188,7 +208,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS)
                     phase = 2;
                 }
             } else if (PAR) {
-                if (uniform(rng, R(0)) * sm < sigma) {
+                if (u2 * sm < sigma) {
                     flight_done = true;
                     collided = true;
                 }
@@ -299,9 +319,11 @@ __global__ void k_delta_track_batch(const DevScene S, BatchParams B) {
         t -= step_len(rng, inv);
         if (t > t1) return;
         R x[3] = {o[0] + d[0] * t, o[1] + d[1] * t, o[2] + d[2] * t};
+        const R u2 = uniform(rng, R(0));
+        if (u2 * sm >= (R)cell_bound(S, x)) continue;  // certain null collision
         const R s = sample(S, x);
         const R sigma = density(S, R(0)) * tf_alpha(S, s);
-        if (uniform(rng, R(0)) * sm < sigma) {
+        if (u2 * sm < sigma) {
             B.hit[i] = 1;
             if (B.pos3)
                 for (int a = 0; a < 3; ++a) B.pos3[3 * i + a] = (double)x[a];
@@ -348,8 +370,10 @@ __global__ void k_transmittance_batch(const DevScene S, BatchParams B) {
             t -= log(1.0 - pcg_double(rng)) * inv;
             if (t > t1) break;
             double x[3] = {a[0] + dir[0] * t, a[1] + dir[1] * t, a[2] + dir[2] * t};
+            const double u2 = pcg_double(rng);
+            if (u2 * S.sigma_max >= cell_bound(S, x)) continue;  // certain null collision
             const double sigma = S.density_scale * tf_alpha_d(S, sample_d(S, x));
-            if (pcg_double(rng) * S.sigma_max < sigma) {
+            if (u2 * S.sigma_max < sigma) {
                 collided = true;
                 break;
             }

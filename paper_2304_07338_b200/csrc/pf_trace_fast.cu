@@ -19,48 +19,52 @@
 
 namespace pfk {
 
+// DDA state in named scalars (no dynamic indexing -> stays in registers).
 struct Dda {
-    int c[3];        // current macro cell
-    int step[3];     // +1 / -1
-    float tm[3];     // ray parameter of the next boundary crossing per axis
-    float td[3];     // parameter increment per cell per axis
+    int cell;                  // linear macro-cell index
+    int cx, cy, cz;            // macro cell coordinates
+    int sx, sy, sz;            // +1 / -1 / 0
+    float tmx, tmy, tmz;       // ray parameter of the next boundary crossing per axis
+    float tdx, tdy, tdz;       // parameter increment per cell per axis
 };
 
-__device__ __forceinline__ void dda_init(const DevScene &S, const float o[3], const float d[3], float t, Dda &D) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const float p = fmaf(d[a], t, o[a]);
-        int ci = (int)floorf(p * S.minv_h[a]);
-        ci = min(max(ci, 0), S.mc[a] - 1);
-        D.c[a] = ci;
-        const float inv = 1.0f / d[a];  // +-inf for axis-parallel rays
-        if (d[a] > 0.0f) {
-            D.step[a] = 1;
-            D.tm[a] = ((float)(ci + 1) * S.mh[a] - o[a]) * inv;
-            D.td[a] = S.mh[a] * inv;
-        } else if (d[a] < 0.0f) {
-            D.step[a] = -1;
-            D.tm[a] = ((float)ci * S.mh[a] - o[a]) * inv;
-            D.td[a] = -S.mh[a] * inv;
-        } else {
-            D.step[a] = 0;
-            D.tm[a] = __int_as_float(0x7f800000);
-            D.td[a] = __int_as_float(0x7f800000);
-        }
+__device__ __forceinline__ void dda_axis(float o, float d, float t, float minv_h, float mh, int mc, int &c, int &st,
+                                         float &tm, float &td) {
+    const float p = fmaf(d, t, o);
+    c = min(max((int)floorf(p * minv_h), 0), mc - 1);
+    const float inv = 1.0f / d;  // +-inf for axis-parallel rays
+    if (d > 0.0f) {
+        st = 1;
+        tm = ((float)(c + 1) * mh - o) * inv;
+        td = mh * inv;
+    } else if (d < 0.0f) {
+        st = -1;
+        tm = ((float)c * mh - o) * inv;
+        td = -mh * inv;
+    } else {
+        st = 0;
+        tm = __int_as_float(0x7f800000);
+        td = __int_as_float(0x7f800000);
     }
+}
+
+__device__ __forceinline__ void dda_init(const DevScene &S, const float o[3], const float d[3], float t, Dda &D) {
+    dda_axis(o[0], d[0], t, S.minv_h[0], S.mh[0], S.mc[0], D.cx, D.sx, D.tmx, D.tdx);
+    dda_axis(o[1], d[1], t, S.minv_h[1], S.mh[1], S.mc[1], D.cy, D.sy, D.tmy, D.tdy);
+    dda_axis(o[2], d[2], t, S.minv_h[2], S.mh[2], S.mc[2], D.cz, D.sz, D.tmz, D.tdz);
+    D.cell = D.cx + S.mc[0] * (D.cy + S.mc[1] * D.cz);
 }
 
 // Spend optical depth tau through the majorant grid from t.  Returns true at a
 // tentative collision (t updated, m = that cell's majorant); false when the
 // flight reaches t1 first.
 __device__ __forceinline__ bool dda_advance(const DevScene &S, Dda &D, float &t, float t1, float &tau, float &m) {
+    const int stride_y = S.mc[0], stride_z = S.mc[0] * S.mc[1];
     for (;;) {
-        const int cell = D.c[0] + S.mc[0] * (D.c[1] + S.mc[1] * D.c[2]);
-        m = __ldg(S.maj + cell);
-        const int ax = (D.tm[0] < D.tm[1]) ? (D.tm[0] < D.tm[2] ? 0 : 2) : (D.tm[1] < D.tm[2] ? 1 : 2);
-        const float t_exit = fminf(D.tm[ax], t1);
-        const float seg = t_exit - t;
-        const float od = m * seg;
+        m = __ldg(S.maj + D.cell);
+        const float tn = fminf(D.tmx, fminf(D.tmy, D.tmz));
+        const float t_exit = fminf(tn, t1);
+        const float od = m * (t_exit - t);
         if (od >= tau && m > 0.0f) {
             t += tau / m;
             return true;
@@ -68,15 +72,28 @@ __device__ __forceinline__ bool dda_advance(const DevScene &S, Dda &D, float &t,
         tau -= od;
         t = t_exit;
         if (t_exit >= t1) return false;
-        D.c[ax] += D.step[ax];
-        if (D.c[ax] < 0 || D.c[ax] >= S.mc[ax]) return false;
-        D.tm[ax] += D.td[ax];
+        if (D.tmx == tn) {
+            D.cx += D.sx;
+            if ((unsigned)D.cx >= (unsigned)S.mc[0]) return false;
+            D.cell += D.sx;
+            D.tmx += D.tdx;
+        } else if (D.tmy == tn) {
+            D.cy += D.sy;
+            if ((unsigned)D.cy >= (unsigned)S.mc[1]) return false;
+            D.cell += D.sy * stride_y;
+            D.tmy += D.tdy;
+        } else {
+            D.cz += D.sz;
+            if ((unsigned)D.cz >= (unsigned)S.mc[2]) return false;
+            D.cell += D.sz * stride_z;
+            D.tmz += D.tdz;
+        }
     }
 }
 
 __device__ __forceinline__ float sample_tau(Pcg &r) { return -__logf(pcg_one_minus_u_f(r)); }
 
-__global__ void __launch_bounds__(PF_TRACE_THREADS) k_render_trace_fast(const DevScene S, const TraceParams P) {
+__global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const DevScene S, const TraceParams P) {
     float *slots = reinterpret_cast<float *>(P.slots);
     const float ds = S.density_scale_f;
     const float g = (float)P.g;
