@@ -367,16 +367,43 @@ size_t or_field_param_count(const or_field_cfg *c) {
 }
 
 /* Multilinear hashgrid lookup of one input. */
+/* Per-level constants, memoised per thread (they only depend on the config). */
+typedef struct {
+    or_hashgrid_cfg cfg;
+    int valid;
+    int N[64];
+    uint32_t size[64];
+    int dense[64];
+} or_level_cache;
+static _Thread_local or_level_cache g_level_cache[2];
+
+static const or_level_cache *or_levels(const or_hashgrid_cfg *c) {
+    or_level_cache *lc = &g_level_cache[c->dims == 3 ? 0 : 1];
+    if (!lc->valid || lc->cfg.dims != c->dims || lc->cfg.levels != c->levels ||
+        lc->cfg.features != c->features || lc->cfg.base_res != c->base_res ||
+        lc->cfg.growth != c->growth || lc->cfg.log2_table != c->log2_table) {
+        for (int l = 0; l < c->levels && l < 64; ++l) {
+            lc->N[l] = or_hashgrid_level_res(c, l);
+            lc->size[l] = or_hashgrid_level_size(c, l);
+            lc->dense[l] = or_hashgrid_level_dense(c, l);
+        }
+        lc->cfg = *c;
+        lc->valid = 1;
+    }
+    return lc;
+}
+
 static void or_hashgrid_encode(const or_hashgrid_cfg *c, const float *table, const double *in,
                                double *out) {
     static const uint32_t primes[3] = {1u, 2654435761u, 805459861u};
     const int d = c->dims, F = c->features;
     const uint32_t Tmask = (1u << c->log2_table) - 1u;
+    const or_level_cache *lc = or_levels(c);
     size_t off = 0;
     for (int l = 0; l < c->levels; ++l) {
-        const int N = or_hashgrid_level_res(c, l);
-        const uint32_t size = or_hashgrid_level_size(c, l);
-        const int dense = or_hashgrid_level_dense(c, l);
+        const int N = lc->N[l];
+        const uint32_t size = lc->size[l];
+        const int dense = lc->dense[l];
         int ci[3];
         double f[3];
         for (int i = 0; i < d; ++i) {

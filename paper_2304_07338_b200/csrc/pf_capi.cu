@@ -1023,6 +1023,8 @@ int pf_knn_build(pf_ctx *c, const pf_photon *photons, size_t n, int n_phases, co
     if (int e = (int)knn_sort((const PhotonRec *)c->k_photons.p, n, K, c->kb, c->stream))
         return set_err(PF_ERR_RUNTIME, "knn build: %s", cudaGetErrorString((cudaError_t)e));
     K.spos = (const float4 *)c->kb.spos.p;
+    K.spay = (const float4 *)c->kb.spay.p;
+    K.inv = (const uint32_t *)c->kb.inv.p;
     K.cell_start = (const uint32_t *)c->kb.cell_start.p;
     K.photons = (const PhotonRec *)c->k_photons.p;
     c->knn = K;

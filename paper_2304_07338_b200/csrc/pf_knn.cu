@@ -70,12 +70,19 @@ __global__ void k_knn_keys(const PhotonRec *ph, size_t n, const KnnParams P, uin
     vals[i] = (uint32_t)i;
 }
 
-__global__ void k_knn_gather(const PhotonRec *ph, size_t n, const uint32_t *vals, float4 *spos) {
+// Sorted copies in (phase, cell, id) order: positions + id for the candidate
+// scan, {direction, power} payload for Eq. 6 (a query's neighbours sit in a
+// few cells, so their payloads are contiguous), and the id -> sorted-index map.
+__global__ void k_knn_gather(const PhotonRec *ph, size_t n, const uint32_t *vals, float4 *spos, float4 *spay,
+                             uint32_t *inv) {
     const size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const uint32_t id = vals[j];
     const PhotonRec p = ph[id];
     spos[j] = make_float4(p.position[0], p.position[1], p.position[2], __uint_as_float(id));
+    spay[2 * j] = make_float4(p.direction[0], p.direction[1], p.direction[2], p.power[0]);
+    spay[2 * j + 1] = make_float4(p.power[1], p.power[2], 0.0f, 0.0f);
+    inv[id] = (uint32_t)j;
 }
 
 // ---- query ---------------------------------------------------------------
@@ -92,6 +99,43 @@ struct WarpTopK {
         for (int s = 0; s < KP; ++s)
             if (s == (p >> 5)) r = v[s];
         return __shfl_sync(0xffffffffu, r, p & 31);
+    }
+    // Merge up to 32 new keys (one per lane, ~0ull = none) in one pass:
+    // bitonic-sort them across the warp, take min(list, reversed(new)) on the
+    // last slot (the union's KP*32 smallest as a bitonic sequence), then a
+    // bitonic merge over the KP*32 positions.  Exact; keys are distinct.
+    __device__ __forceinline__ void merge32(uint64_t x, unsigned lane) {
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
+                const bool up = (lane & k) == 0 || k == 32;
+                const bool lower = (lane & j) == 0;
+                x = (lower == up) ? (x < y ? x : y) : (x < y ? y : x);
+            }
+        }
+        const uint64_t br = __shfl_sync(0xffffffffu, x, 31 - lane);
+        v[KP - 1] = v[KP - 1] < br ? v[KP - 1] : br;
+#pragma unroll
+        for (int J = KP / 2; J >= 1; J >>= 1) {
+#pragma unroll
+            for (int s = 0; s < KP; ++s)
+                if ((s & J) == 0) {
+                    const uint64_t a = v[s], b = v[s + J];
+                    v[s] = a < b ? a : b;
+                    v[s + J] = a < b ? b : a;
+                }
+        }
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+            const bool lower = (lane & j) == 0;
+#pragma unroll
+            for (int s = 0; s < KP; ++s) {
+                const uint64_t y = __shfl_xor_sync(0xffffffffu, v[s], j);
+                v[s] = lower ? (v[s] < y ? v[s] : y) : (v[s] < y ? y : v[s]);
+            }
+        }
     }
     __device__ __forceinline__ void insert(uint64_t key, unsigned lane) {
         int pos = 0;
@@ -138,40 +182,50 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
     const float r2 = P.r2;
 
     if (g < P.n_phases && P.grid[g].n > 0) {
-        const KnnGrid &G = P.grid[g];
-        int qc[3];
+        // register copy of this phase's grid (no dynamically indexed param loads)
+        const KnnGrid &Gp = P.grid[g];
+        int R[3], qc[3];
+        float lo[3], h[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) qc[a] = cell_axis((double)q[a], G.lo[a], G.inv_h[a], G.R[a]);
-        const int rmax = max(G.R[0], max(G.R[1], G.R[2]));
+        for (int a = 0; a < 3; ++a) {
+            R[a] = Gp.R[a];
+            lo[a] = (float)Gp.lo[a];
+            h[a] = (float)Gp.h[a];
+            qc[a] = cell_axis((double)q[a], Gp.lo[a], Gp.inv_h[a], R[a]);
+        }
+        const float eps = (float)Gp.eps + 1e-6f;  // box slack >> binary32 rounding of the bounds
+        const uint32_t cbase = Gp.cell_base;
+        const double hmin = Gp.hmin, geps = Gp.eps;
+        // 1-D gap between the query and cell c along an axis (edge cells unbounded)
+        auto gap = [&](int a, int c) -> float {
+            const float l = c == 0 ? -3.0e38f : fmaf((float)c, h[a], lo[a]) - eps;
+            const float u = c == R[a] - 1 ? 3.0e38f : fmaf((float)(c + 1), h[a], lo[a]) + eps;
+            const float d = q[a] < l ? l - q[a] : (q[a] > u ? q[a] - u : 0.0f);
+            return d * d;
+        };
+        float kth = __int_as_float(0x7f800000);  // d2 of the K-th entry
+        const int rmax = max(R[0], max(R[1], R[2]));
         for (int ring = 0; ring <= rmax; ++ring) {
             for (int dz = -ring; dz <= ring; ++dz) {
                 const int cz = qc[2] + dz;
-                if (cz < 0 || cz >= G.R[2]) continue;
+                if (cz < 0 || cz >= R[2]) continue;
+                const float gz = gap(2, cz);
+                if (gz * (1.0f - 1e-5f) > fminf(r2, kth)) continue;
                 for (int dy = -ring; dy <= ring; ++dy) {
                     const int cy = qc[1] + dy;
-                    if (cy < 0 || cy >= G.R[1]) continue;
+                    if (cy < 0 || cy >= R[1]) continue;
+                    const float gyz = gz + gap(1, cy);
+                    if (gyz * (1.0f - 1e-5f) > fminf(r2, kth)) continue;
                     const bool yz_shell = abs(dz) == ring || abs(dy) == ring;
-                    for (int dx = -ring; dx <= ring; dx += (yz_shell ? 1 : 2 * max(ring, 1))) {
+                    const int step = yz_shell ? 1 : 2 * max(ring, 1);
+                    const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
+                    for (int dx = -ring; dx <= ring; dx += step) {
                         const int cx = qc[0] + dx;
-                        if (cx < 0 || cx >= G.R[0]) continue;
-                        const int c3[3] = {cx, cy, cz};
-                        // conservative box distance (expanded by eps_abs; edge cells unbounded)
-                        double lb = 0.0;
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) {
-                            const double lo = c3[a] == 0 ? -1e300 : G.lo[a] + c3[a] * G.h[a] - G.eps;
-                            const double hi = c3[a] == G.R[a] - 1 ? 1e300
-                                                                  : G.lo[a] + (c3[a] + 1) * G.h[a] + G.eps;
-                            const double dq = (double)q[a];
-                            const double d = dq < lo ? lo - dq : (dq > hi ? dq - hi : 0.0);
-                            lb += d * d;
-                        }
-                        lb *= (1.0 - 1e-5);
-                        if (lb > (double)r2) continue;
-                        if (count >= K && lb > (double)__uint_as_float((uint32_t)(thr >> 32))) continue;
-                        const uint32_t cell =
-                            G.cell_base + (uint32_t)cx + (uint32_t)G.R[0] * ((uint32_t)cy + (uint32_t)G.R[1] * (uint32_t)cz);
-                        const uint32_t b = P.cell_start[cell], e = P.cell_start[cell + 1];
+                        if (cx < 0 || cx >= R[0]) continue;
+                        const float lb = (gyz + gap(0, cx)) * (1.0f - 1e-5f);
+                        if (lb > r2 || (count >= K && lb > kth)) continue;
+                        const uint32_t cell = row + (uint32_t)cx;
+                        const uint32_t b = __ldg(P.cell_start + cell), e = __ldg(P.cell_start + cell + 1);
                         for (uint32_t j0 = b; j0 < e; j0 += 32) {
                             const uint32_t j = j0 + lane;
                             uint64_t key = ~0ull;
@@ -181,12 +235,24 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
                                 if (d2 <= r2) key = ((uint64_t)__float_as_uint(d2) << 32) | __float_as_uint(c.w);
                             }
                             unsigned m = __ballot_sync(0xffffffffu, key < thr);
+                            if (__popc(m) >= 4) {  // bulk path
+                                top.merge32(key < thr ? key : ~0ull, lane);
+                                count = min(K, count + __popc(m));
+                                if (count >= K) {
+                                    thr = top.at(K - 1);
+                                    kth = __uint_as_float((uint32_t)(thr >> 32));
+                                }
+                                m = 0;
+                            }
                             while (m) {
                                 const int src = __ffs(m) - 1;
                                 const uint64_t k = __shfl_sync(0xffffffffu, key, src);
                                 top.insert(k, lane);
                                 if (count < K) ++count;
-                                if (count >= K) thr = top.at(K - 1);
+                                if (count >= K) {
+                                    thr = top.at(K - 1);
+                                    kth = __uint_as_float((uint32_t)(thr >> 32));
+                                }
                                 m &= ~(1u << src);
                                 m &= __ballot_sync(0xffffffffu, key < thr);
                             }
@@ -194,11 +260,11 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
                     }
                 }
             }
-            // all cells at Chebyshev distance > ring are >= ring*h_min - 2eps away
-            const double bnd = fmax(0.0, ring * G.hmin - 2.0 * G.eps);
+            // every cell at Chebyshev distance > ring is >= ring*h_min - 2 eps away
+            const double bnd = fmax(0.0, ring * hmin - 2.0 * geps);
             const double bnd2 = bnd * bnd * (1.0 - 1e-5);
             if (bnd2 > (double)r2) break;
-            if (count >= K && bnd2 > (double)__uint_as_float((uint32_t)(thr >> 32))) break;
+            if (count >= K && bnd2 > (double)kth) break;
         }
     }
 
@@ -233,12 +299,13 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
                 const int p = s * 32 + (int)lane;
                 double term[3] = {0.0, 0.0, 0.0};
                 if (p < count) {
-                    const PhotonRec ph = P.photons[(uint32_t)top.v[s]];
-                    const double c = w[0] * (double)ph.direction[0] + w[1] * (double)ph.direction[1] +
-                                     w[2] * (double)ph.direction[2];
+                    const uint32_t j = __ldg(P.inv + (uint32_t)top.v[s]);
+                    const float4 a = __ldg(P.spay + 2 * (size_t)j), b = __ldg(P.spay + 2 * (size_t)j + 1);
+                    const double c = w[0] * (double)a.x + w[1] * (double)a.y + w[2] * (double)a.z;
                     const double f = knn_hg_eval(gv, c);
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) term[ch] = f * (double)ph.power[ch];
+                    term[0] = f * (double)a.w;
+                    term[1] = f * (double)b.x;
+                    term[2] = f * (double)b.y;
                 }
                 // sequential sum in list order (bit-identical to the oracle loop)
                 const int n_here = min(32, count - s * 32);
@@ -314,7 +381,8 @@ cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffe
     const size_t ncells = (size_t)P.total_cells + 1;
     if ((e = B.keys.ensure(n * 4)) || (e = B.vals.ensure(n * 4)) || (e = B.keys2.ensure(n * 4)) ||
         (e = B.vals2.ensure(n * 4)) || (e = B.hist.ensure(ncells * 4)) ||
-        (e = B.cell_start.ensure((ncells + 1) * 4)) || (e = B.spos.ensure(n * 16)))
+        (e = B.cell_start.ensure((ncells + 1) * 4)) || (e = B.spos.ensure(n * 16)) ||
+        (e = B.spay.ensure(n * 32)) || (e = B.inv.ensure(n * 4)))
         return e;
     cudaMemsetAsync(B.hist.p, 0, ncells * 4, st);
     if (n) {
@@ -339,7 +407,8 @@ cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffe
                                   (int)ncells, st);
     if (n) {
         k_knn_gather<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ph, n, (const uint32_t *)B.vals2.p,
-                                                                  (float4 *)B.spos.p);
+                                                                  (float4 *)B.spos.p, (float4 *)B.spay.p,
+                                                                  (uint32_t *)B.inv.p);
         if ((e = cudaGetLastError())) return e;
     }
     return cudaSuccess;

@@ -33,6 +33,8 @@ struct KnnParams {
     KnnGrid grid[PF_MAX_PHASES];
     double phase[PF_MAX_PHASES];
     const float4 *spos;           // sorted {x, y, z, id}
+    const float4 *spay;           // sorted {dir xyz, power r} {power g, b, -, -}
+    const uint32_t *inv;          // id -> sorted index
     const uint32_t *cell_start;   // total_cells + 1
     const PhotonRec *photons;     // load order (ids)
     size_t nq;
@@ -49,7 +51,7 @@ struct KnnParams {
 };
 
 struct KnnBuffers {
-    DevBuf keys, vals, keys2, vals2, hist, cell_start, spos, temp, temp2;
+    DevBuf keys, vals, keys2, vals2, hist, cell_start, spos, spay, inv, temp, temp2;
 };
 
 cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins, uint32_t *maxs,
