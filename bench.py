@@ -300,8 +300,8 @@ def main():
 
     # ---- extras (rank 0): field-query throughput (part c) and KNN gather (config 3)
     extras = {}
-    if rank == 0 and not args.no_extras:
-        extras = bench_extras(ctx, fc, params, peaks)
+    if not args.no_extras:  # every rank runs its own query shard; rank 0 reports the aggregate
+        extras = bench_extras(ctx, fc, params, peaks, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -348,14 +348,28 @@ def main():
             **extras,
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
-def bench_extras(ctx, fc, params, peaks):
-    """Part (c) field-query throughput and the config-3 KNN gather (secondary lines)."""
+def _sum_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def bench_extras(ctx, fc, params, peaks, rank=0, world=1):
+    """Part (c) photon-field queries/s and the config-3 KNN gather, aggregated
+    over the ranks (each rank answers its own 2^22 / 2^20 query shard against
+    the replicated field / photon map; weak scaling)."""
     import torch
     out = {}
     n = 1 << 22
@@ -374,30 +388,29 @@ def bench_extras(ctx, fc, params, peaks):
     b.record()
     torch.cuda.synchronize()
     dt = a.elapsed_time(b) / 5 / 1e3
+    qps_rank = n / dt
     din = fc.pos.levels * fc.pos.features + fc.dir.levels * fc.dir.features + 1
     flop = 2 * (din * 64 + (fc.hidden_layers - 1) * 64 * 64 + 64 * 3)
-    qps = n / dt
-    out["field_query"] = {"queries_per_s": qps, "n": n, "flop_per_query": flop,
+    qps = _sum_over_ranks(qps_rank, world)
+    out["field_query"] = {"queries_per_s": qps, "n_per_rank": n, "ranks": world, "scaling": "weak",
+                          "flop_per_query": flop,
                           "roofline": {"bound": "tensor", "achieved": qps * flop / 1e12,
-                                       "peak": float(peaks["bf16_tflops"]), "unit": "TFLOP/s",
-                                       "frac": qps * flop / 1e12 / float(peaks["bf16_tflops"])},
+                                       "peak": float(peaks["bf16_tflops"]) * world, "unit": "TFLOP/s",
+                                       "frac": qps * flop / 1e12 / (float(peaks["bf16_tflops"]) * world)},
                           "gather_bytes_per_query": 2 * (fc.pos.levels * 8 * fc.pos.features +
                                                          fc.dir.levels * 4 * fc.dir.features)}
-    # config 3: KNN radiance estimate, k = 64 over a 4M-photon 3-phase map
-    from paper_2304_07338_b200.scene import synth_photons
-    ph = synth_photons(4_000_000, 3, seed=3)
-    ph["power"] *= 1e-4
-    ctx.knn_build(ph, [-0.75, 0.0, 0.75])
-    batch = 1 << 16
-    for _ in range(2):
-        ctx.make_batch(seed=1, step=0, batch=batch, K=64)
-    t0 = time.perf_counter()
-    steps = 5
-    for s in range(steps):
-        ctx.make_batch(seed=1, step=s, batch=batch, K=64)
-    dt = (time.perf_counter() - t0) / steps
-    out["knn_gather"] = {"queries_per_s": batch / dt, "batch": batch, "K": 64, "photons": 4_000_000,
-                         "note": "make_batch incl. host copies of the batch; ids bit-exact"}
+    # config 3: KNN radiance estimate (k = 64) over a 4M-photon 3-phase map,
+    # 2^20 device-resident queries per batch, CUDA-event timed
+    sys.path.insert(0, str(ROOT / "tools"))
+    import bench_knn
+    k = bench_knn.run(ctx)
+    k["queries_per_s"] = _sum_over_ranks(k["queries_per_s"], world)
+    k["algorithmic_GBps"] = _sum_over_ranks(k["algorithmic_GBps"], world)
+    k["ranks"], k["scaling"] = world, "weak"
+    hbm = float(peaks["hbm_gbs"]) * world
+    k["roofline"] = {"bound": "hbm", "achieved": k["algorithmic_GBps"], "peak": hbm, "unit": "GB/s",
+                     "frac": k["algorithmic_GBps"] / hbm, "per_unit": "2560 B (K=64 x 40-B records) per query"}
+    out["knn_gather"] = k
     return out
 
 
