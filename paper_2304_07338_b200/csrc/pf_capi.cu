@@ -119,6 +119,13 @@ int macro_default() {
     return v >= 2 && v <= 64 ? v : PF_MACRO;
 }
 
+// Target photons of one phase per KNN grid cell (PF_KNN_PPC overrides it for tuning sweeps).
+double knn_photons_per_cell() {
+    const char *e = std::getenv("PF_KNN_PPC");
+    const double v = e ? std::atof(e) : 0.0;
+    return v > 0.05 && v < 1024.0 ? v : 8.0;
+}
+
 }  // namespace
 
 struct pf_ctx {
@@ -996,7 +1003,7 @@ int pf_knn_build(pf_ctx *c, const pf_photon *photons, size_t n, int n_phases, co
             vol *= ext[a];
         }
         // ~8 photons of this phase per cell (K=64 reaches its K-th within ~1.2 cells)
-        double h = std::cbrt(8.0 * vol / (double)G.n);
+        double h = std::cbrt(knn_photons_per_cell() * vol / (double)G.n);
         uint64_t cells = 1;
         for (int a = 0; a < 3; ++a) {
             G.R[a] = (int)std::min(1024.0, std::max(1.0, std::ceil(ext[a] / h)));
@@ -1063,6 +1070,8 @@ static int knn_run(pf_ctx *c, size_t nq, const float *x3, const double *w3, cons
     P.out_d2 = (float *)dd2;
     P.out_counts = (int32_t *)dcnt;
     P.out_targets = (double *)dout;
+    P.order = nullptr;
+    if (nq >= 4096) PF_CUDA(knn_order(P.qx, P.qg, nq, c->kb, &P.order, c->stream));
     PF_CUDA(knn_query(P, c->stream));
     if (hi) PF_CUDA(cudaMemcpyAsync(ids, dids, nq * K * 4, cudaMemcpyDeviceToHost, c->stream));
     if (hd) PF_CUDA(cudaMemcpyAsync(d2, dd2, nq * K * 4, cudaMemcpyDeviceToHost, c->stream));

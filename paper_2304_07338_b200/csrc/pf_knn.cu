@@ -86,6 +86,12 @@ __global__ void k_knn_gather(const PhotonRec *ph, size_t n, const uint32_t *vals
 }
 
 // ---- query ---------------------------------------------------------------
+__device__ __forceinline__ unsigned knn_lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
 template <int KP>
 struct WarpTopK {
     uint64_t v[KP];  // list position p = s*32 + lane, ascending
@@ -169,9 +175,13 @@ __device__ __forceinline__ double knn_hg_eval(double g, double c) {
 
 template <int KP>
 __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
+    // per-warp staging buffer: accepted candidates are merged 32 at a time
+    __shared__ uint64_t s_buf[4][32];
     const unsigned lane = threadIdx.x & 31u;
-    const size_t qi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (qi >= P.nq) return;
+    uint64_t *buf = s_buf[(threadIdx.x >> 5) & 3];
+    const size_t qs = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (qs >= P.nq) return;
+    const size_t qi = P.order ? (size_t)__ldg(P.order + qs) : qs;  // spatially sorted visit order
     const int K = P.K;
     const float q[3] = {P.qx[3 * qi], P.qx[3 * qi + 1], P.qx[3 * qi + 2]};
     const int g = P.qg[qi];
@@ -179,7 +189,42 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
     top.init();
     int count = 0;
     uint64_t thr = ~0ull;  // key of the K-th entry (inf while count < K)
+    float kth = __int_as_float(0x7f800000);
     const float r2 = P.r2;
+    int nb = 0;  // keys staged in buf (warp-uniform)
+
+    auto flush = [&]() {
+        __syncwarp();
+        const uint64_t x = (int)lane < nb ? buf[lane] : ~0ull;
+        __syncwarp();
+        top.merge32(x, lane);
+        count = min(K, count + nb);
+        nb = 0;
+        if (count >= K) {
+            thr = top.at(K - 1);
+            kth = __uint_as_float((uint32_t)(thr >> 32));
+        }
+    };
+    // scan the contiguous sorted records [b, e) (one row segment of cells)
+    auto scan = [&](uint32_t b, uint32_t e) {
+        for (uint32_t j0 = b; j0 < e; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            uint64_t key = ~0ull;
+            if (j < e) {
+                const float4 c = __ldg(&P.spos[j]);
+                const float d2 = d2_rn(c, q);
+                if (d2 <= r2) key = ((uint64_t)__float_as_uint(d2) << 32) | __float_as_uint(c.w);
+            }
+            const bool acc = key < thr;
+            const unsigned m = __ballot_sync(0xffffffffu, acc);
+            const int nn = __popc(m);
+            if (nn == 0) continue;
+            if (nb + nn > 32) flush();
+            if (acc) buf[nb + __popc(m & knn_lanemask_lt())] = key;
+            nb += nn;
+            if (nb == 32) flush();
+        }
+    };
 
     if (g < P.n_phases && P.grid[g].n > 0) {
         // register copy of this phase's grid (no dynamically indexed param loads)
@@ -196,70 +241,42 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
         const float eps = (float)Gp.eps + 1e-6f;  // box slack >> binary32 rounding of the bounds
         const uint32_t cbase = Gp.cell_base;
         const double hmin = Gp.hmin, geps = Gp.eps;
-        // 1-D gap between the query and cell c along an axis (edge cells unbounded)
-        auto gap = [&](int a, int c) -> float {
-            const float l = c == 0 ? -3.0e38f : fmaf((float)c, h[a], lo[a]) - eps;
-            const float u = c == R[a] - 1 ? 3.0e38f : fmaf((float)(c + 1), h[a], lo[a]) + eps;
+        // squared 1-D gap between the query and the cell interval [c0, c1] on axis a
+        // (edge cells extend to infinity: clamped photons may lie outside the grid box)
+        auto gap = [&](int a, int c0, int c1) -> float {
+            const float l = c0 == 0 ? -3.0e38f : fmaf((float)c0, h[a], lo[a]) - eps;
+            const float u = c1 == R[a] - 1 ? 3.0e38f : fmaf((float)(c1 + 1), h[a], lo[a]) + eps;
             const float d = q[a] < l ? l - q[a] : (q[a] > u ? q[a] - u : 0.0f);
             return d * d;
         };
-        float kth = __int_as_float(0x7f800000);  // d2 of the K-th entry
         const int rmax = max(R[0], max(R[1], R[2]));
         for (int ring = 0; ring <= rmax; ++ring) {
             for (int dz = -ring; dz <= ring; ++dz) {
                 const int cz = qc[2] + dz;
                 if (cz < 0 || cz >= R[2]) continue;
-                const float gz = gap(2, cz);
-                if (gz * (1.0f - 1e-5f) > fminf(r2, kth)) continue;
+                const float gz = gap(2, cz, cz);
                 for (int dy = -ring; dy <= ring; ++dy) {
                     const int cy = qc[1] + dy;
                     if (cy < 0 || cy >= R[1]) continue;
-                    const float gyz = gz + gap(1, cy);
+                    const float gyz = gz + gap(1, cy, cy);
                     if (gyz * (1.0f - 1e-5f) > fminf(r2, kth)) continue;
-                    const bool yz_shell = abs(dz) == ring || abs(dy) == ring;
-                    const int step = yz_shell ? 1 : 2 * max(ring, 1);
                     const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
-                    for (int dx = -ring; dx <= ring; dx += step) {
-                        const int cx = qc[0] + dx;
-                        if (cx < 0 || cx >= R[0]) continue;
-                        const float lb = (gyz + gap(0, cx)) * (1.0f - 1e-5f);
-                        if (lb > r2 || (count >= K && lb > kth)) continue;
-                        const uint32_t cell = row + (uint32_t)cx;
-                        const uint32_t b = __ldg(P.cell_start + cell), e = __ldg(P.cell_start + cell + 1);
-                        for (uint32_t j0 = b; j0 < e; j0 += 32) {
-                            const uint32_t j = j0 + lane;
-                            uint64_t key = ~0ull;
-                            if (j < e) {
-                                const float4 c = __ldg(&P.spos[j]);
-                                const float d2 = d2_rn(c, q);
-                                if (d2 <= r2) key = ((uint64_t)__float_as_uint(d2) << 32) | __float_as_uint(c.w);
-                            }
-                            unsigned m = __ballot_sync(0xffffffffu, key < thr);
-                            if (__popc(m) >= 4) {  // bulk path
-                                top.merge32(key < thr ? key : ~0ull, lane);
-                                count = min(K, count + __popc(m));
-                                if (count >= K) {
-                                    thr = top.at(K - 1);
-                                    kth = __uint_as_float((uint32_t)(thr >> 32));
-                                }
-                                m = 0;
-                            }
-                            while (m) {
-                                const int src = __ffs(m) - 1;
-                                const uint64_t k = __shfl_sync(0xffffffffu, key, src);
-                                top.insert(k, lane);
-                                if (count < K) ++count;
-                                if (count >= K) {
-                                    thr = top.at(K - 1);
-                                    kth = __uint_as_float((uint32_t)(thr >> 32));
-                                }
-                                m &= ~(1u << src);
-                                m &= __ballot_sync(0xffffffffu, key < thr);
-                            }
-                        }
+                    // the ring's new cells in this row: the whole [-ring, ring] segment on
+                    // the outer y/z faces, else only the two end cells
+                    const bool face = abs(dz) == ring || abs(dy) == ring;
+                    for (int part = 0; part < (face ? 1 : 2); ++part) {
+                        int x0 = face ? qc[0] - ring : (part == 0 ? qc[0] - ring : qc[0] + ring);
+                        int x1 = face ? qc[0] + ring : x0;
+                        x0 = max(x0, 0);
+                        x1 = min(x1, R[0] - 1);
+                        if (x0 > x1) continue;
+                        const float lb = (gyz + gap(0, x0, x1)) * (1.0f - 1e-5f);
+                        if (lb > r2 || lb > kth) continue;
+                        scan(__ldg(P.cell_start + row + (uint32_t)x0), __ldg(P.cell_start + row + (uint32_t)x1 + 1));
                     }
                 }
             }
+            if (nb) flush();
             // every cell at Chebyshev distance > ring is >= ring*h_min - 2 eps away
             const double bnd = fmax(0.0, ring * hmin - 2.0 * geps);
             const double bnd2 = bnd * bnd * (1.0 - 1e-5);
@@ -267,6 +284,7 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
             if (count >= K && bnd2 > (double)kth) break;
         }
     }
+    if (nb) flush();
 
     // ---- outputs: ids / d2 / counts
     if (P.out_ids || P.out_d2) {
@@ -412,6 +430,43 @@ cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffe
         if ((e = cudaGetLastError())) return e;
     }
     return cudaSuccess;
+}
+
+// (phase, 30-bit Morton code of the position in [0,1]^3) visit-order keys
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_knn_order_keys(const float *x3, const uint8_t *g, size_t n, uint32_t *keys, uint32_t *idx) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = (uint32_t)(__saturatef(x3[3 * i + a]) * 1023.0f);
+    keys[i] = ((uint32_t)min((int)g[i], 3) << 30) | (spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2));
+    idx[i] = (uint32_t)i;
+}
+
+cudaError_t knn_order(const float *x3, const uint8_t *g, size_t n, KnnBuffers &B, const uint32_t **order,
+                      cudaStream_t st) {
+    cudaError_t e;
+    if ((e = B.qk.ensure(n * 4)) || (e = B.qi.ensure(n * 4)) || (e = B.qk2.ensure(n * 4)) || (e = B.qi2.ensure(n * 4)))
+        return e;
+    k_knn_order_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x3, g, n, (uint32_t *)B.qk.p, (uint32_t *)B.qi.p);
+    if ((e = cudaGetLastError())) return e;
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, (uint32_t *)B.qk.p, (uint32_t *)B.qk2.p, (uint32_t *)B.qi.p,
+                                    (uint32_t *)B.qi2.p, (int)n, 0, 32, st);
+    if ((e = B.temp3.ensure(tmp + 256))) return e;
+    cub::DeviceRadixSort::SortPairs(B.temp3.p, tmp, (uint32_t *)B.qk.p, (uint32_t *)B.qk2.p, (uint32_t *)B.qi.p,
+                                    (uint32_t *)B.qi2.p, (int)n, 0, 32, st);
+    *order = (const uint32_t *)B.qi2.p;
+    return cudaGetLastError();
 }
 
 cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {

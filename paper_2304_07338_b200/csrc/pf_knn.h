@@ -38,6 +38,7 @@ struct KnnParams {
     const uint32_t *cell_start;   // total_cells + 1
     const PhotonRec *photons;     // load order (ids)
     size_t nq;
+    const uint32_t *order;        // optional visit order (spatially sorted queries)
     const float *qx;
     const uint8_t *qg;
     const double *qw;
@@ -52,6 +53,7 @@ struct KnnParams {
 
 struct KnnBuffers {
     DevBuf keys, vals, keys2, vals2, hist, cell_start, spos, spay, inv, temp, temp2;
+    DevBuf qk, qi, qk2, qi2, temp3;  // query visit-order sort
 };
 
 cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins, uint32_t *maxs,
@@ -59,6 +61,8 @@ cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins
 cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffers &B,
                      cudaStream_t st);
 cudaError_t knn_query(const KnnParams &P, cudaStream_t st);
+cudaError_t knn_order(const float *x3, const uint8_t *g, size_t n, KnnBuffers &B, const uint32_t **order,
+                      cudaStream_t st);
 cudaError_t knn_make_queries(uint64_t initstate, uint64_t base, size_t batch, int n_phases,
                              float *x3, double *w3, uint8_t *gidx, cudaStream_t st);
 
