@@ -335,7 +335,8 @@ def main():
             "frame": {"samples": samples * world, "hits": hits, "hit_fraction": hits / max(samples, 1),
                       "steps_per_sample": steps_tot / max(samples, 1),
                       "ms_trace": tr_ms, "ms_field": fld_ms, "wall_s": wall},
-            "roofline": {"kernel": f"k_render_trace<{args.mode}>", "bound": "hbm",
+            "roofline": {"kernel": "k_render_trace_fast" if args.mode == "fast" else "k_render_trace<parity>",
+                         "bound": "hbm",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "per_unit": "32 B (8 x f32 voxels) per tentative collision, "
