@@ -28,8 +28,38 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+# BASELINE.json configs: c2 is the headline (fits one GPU); c4 / c5 are the
+# multi-GPU shapes, runnable here on N >= 1 GPUs with --config.
+CONFIGS = {
+    "c2": dict(W=1920, H=1080, spp=8, vol=256, dynamic=False,
+               desc="config 2: 256^3 sphere_sinusoid volume (scene A TF, density 100), 1920x1080, 8 spp"),
+    "c4": dict(W=3840, H=2160, spp=16, vol=512, dynamic=False,
+               desc="config 4: 512^3 sphere_sinusoid volume (scene A TF, density 100), 3840x2160, 16 spp"),
+    "c5": dict(W=1920, H=1080, spp=8, vol=1024, dynamic=True,
+               desc="config 5: 1024^3 sphere_sinusoid volume, 1920x1080, 8 spp, transfer function and "
+                    "light changed every frame (majorant grid rebuilt per frame)"),
+}
 W_, H_, SPP, VOL_N, SEED = 1920, 1080, 8, 256, 2024
 METRIC = "frames/s at 1920x1080, 8 spp, 256^3 volume (neural render, Alg. 2)"
+CFG = CONFIGS["c2"]
+
+
+def select_config(name: str) -> None:
+    global W_, H_, SPP, VOL_N, METRIC, CFG
+    CFG = CONFIGS[name]
+    W_, H_, SPP, VOL_N = CFG["W"], CFG["H"], CFG["spp"], CFG["vol"]
+    METRIC = f"frames/s at {W_}x{H_}, {SPP} spp, {VOL_N}^3 volume (neural render, Alg. 2)"
+
+
+def dynamic_scene(i: int, tf0, lights0):
+    """Config 5: per-frame transfer function (alpha ramp scaled) and orbiting light."""
+    import math
+    tf = tf0.copy()
+    tf[:, 4] = np.clip(tf0[:, 4] * (0.75 + 0.25 * math.cos(0.37 * i)), 0.0, 1.0)
+    li = lights0.copy()
+    a = 0.21 * i
+    li[0, 0], li[0, 2] = 0.5 + 2.0 * math.cos(a), 0.5 + 2.0 * math.sin(a)
+    return tf, li
 
 
 def load_peaks():
@@ -167,10 +197,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    select_config(args.config)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -213,7 +245,14 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     ctx.set_timing(True)
 
+    frame_no = [0]
+
     def step(stats=True):
+        if CFG["dynamic"]:  # config 5: new TF + light every frame
+            tf_i, li_i = dynamic_scene(frame_no[0], tf, lights)
+            ctx.set_medium(tf_i, 100.0)
+            ctx.set_lights(li_i)
+        frame_no[0] += 1
         st = ctx.render_neural(cam, rc, out=frame, stats=stats)
         if world > 1:
             ctx.tiles_pack(cam, rc, frame, packed)
@@ -325,9 +364,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if args.mode == "fast" else "f64", "data": "synthetic",
-            "config": {"workload": "config 2: 256^3 sphere_sinusoid volume (scene A TF, density 100), "
-                                   "1920x1080, 8 spp, 1 point light, paper photon field "
-                                   "(16x8 hash grid T=2^19, 5x64 MLP, random init)",
+            "config": {"workload": CFG["desc"] + ", 1 point light, paper photon field "
+                                                 "(16x8 hash grid T=2^19, 5x64 MLP, random init)",
                        "mode": args.mode, "tiles": "16x16 interleaved over ranks",
                        "l2": "flushed (256 MiB write) between timed frames",
                        "parallelism": f"tiles{world}"},

@@ -140,7 +140,7 @@ struct pf_ctx {
     int atlas_log2 = 0;
     int mc[3] = {0, 0, 0};
     int macro = macro_default();  // voxels per macro-cell edge
-    DevBuf macro_mm, maj, tf_dev;
+    DevBuf macro_mm, maj;
     int nx = 0, ny = 0, nz = 0;
     float vmin = 0.f, vmax = 0.f;
     // medium / lights
@@ -416,12 +416,11 @@ int pf_medium_set(pf_ctx *c, const double *tf_pts, int n_pts, double density_sca
     c->sigma_max = sigma_max;
     // per-macro-cell majorants for the FAST tracer
     PF_CUDA(cudaSetDevice(c->device));
-    PF_CUDA(c->tf_dev.ensure(c->tf.size() * sizeof(double)));
-    PF_CUDA(cudaMemcpyAsync(c->tf_dev.p, c->tf.data(), c->tf.size() * sizeof(double), cudaMemcpyHostToDevice,
-                            c->stream));
-    PF_CUDA(launch_macro_majorant((const float2 *)c->macro_mm.p, (size_t)c->mc[0] * c->mc[1] * c->mc[2],
-                                  (const double *)c->tf_dev.p, n_pts, density_scale, (float *)c->maj.p, c->stream));
-    PF_CUDA(cudaStreamSynchronize(c->stream));  // c->tf may be reassigned by the next call
+    TfPoints tp;
+    std::memset(&tp, 0, sizeof(tp));
+    std::memcpy(tp.p, c->tf.data(), c->tf.size() * sizeof(double));
+    PF_CUDA(launch_macro_majorant((const float2 *)c->macro_mm.p, (size_t)c->mc[0] * c->mc[1] * c->mc[2], tp, n_pts,
+                                  density_scale, (float *)c->maj.p, c->stream));
     c->has_medium = true;
     return PF_OK;
 }

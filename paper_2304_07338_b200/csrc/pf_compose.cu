@@ -123,7 +123,8 @@ __global__ void k_macro_minmax(const float *vol, int nx, int ny, int nz, float2 
 }
 
 // majorant = density_scale * TransferFunction::max_alpha(lo, hi) (volume.cpp:163-168), padded 1e-5.
-__device__ double tf_alpha_host_like(const double *p, int n, double s) {
+__device__ double tf_alpha_host_like(const TfPoints &T, int n, double s) {
+    const double *p = T.p;
     s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
     int hi = 1;
     while (hi + 1 < n && p[hi * 5] < s) ++hi;
@@ -132,11 +133,12 @@ __device__ double tf_alpha_host_like(const double *p, int n, double s) {
     return p[(hi - 1) * 5 + 4] + (p[hi * 5 + 4] - p[(hi - 1) * 5 + 4]) * t;
 }
 
-__global__ void k_macro_majorant(const float2 *mm, size_t ncells, const double *tf, int n, double ds, float *maj) {
+__global__ void k_macro_majorant(const float2 *mm, size_t ncells, const TfPoints T, int n, double ds, float *maj) {
+    const double *tf = T.p;
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncells) return;
     const double lo = mm[c].x, hi = mm[c].y;
-    double m = fmax(tf_alpha_host_like(tf, n, lo), tf_alpha_host_like(tf, n, hi));
+    double m = fmax(tf_alpha_host_like(T, n, lo), tf_alpha_host_like(T, n, hi));
     for (int i = 0; i < n; ++i)
         if (tf[5 * i] > lo && tf[5 * i] < hi) m = fmax(m, tf[5 * i + 4]);
     maj[c] = m > 0.0 ? (float)(ds * m * (1.0 + 1e-5)) : 0.0f;
@@ -149,7 +151,7 @@ cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2
     return cudaGetLastError();
 }
 
-cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const double *tf_pts, int n_tf, double ds,
+cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const TfPoints &tf_pts, int n_tf, double ds,
                                   float *maj, cudaStream_t st) {
     k_macro_majorant<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(mm, ncells, tf_pts, n_tf, ds, maj);
     return cudaGetLastError();

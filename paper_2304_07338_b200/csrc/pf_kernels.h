@@ -93,7 +93,11 @@ cudaError_t launch_tiles_unpack(const ComposeParams &C, const float *packed_all,
 int trace_grid_size(bool parity, int device);
 cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy,
                                 int mcz, int macro, cudaStream_t st);
-cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const double *tf_pts, int n_tf,
+// transfer-function control points passed by value (no host->device copy per TF change)
+struct TfPoints {
+    double p[16 * 5];
+};
+cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const TfPoints &tf_pts, int n_tf,
                                   double density_scale, float *maj, cudaStream_t st);
 cudaError_t launch_build_atlas(const float *vol, int nx, int ny, int nz, int log2_cols, float *atlas,
                                size_t aw, size_t ah, cudaStream_t st);

@@ -25,23 +25,26 @@ def synth_volume(kind: str, n: int | tuple[int, int, int]) -> np.ndarray:
     (SPEC.md:683-690), "constant:<v>".
     """
     nx, ny, nz = (n, n, n) if isinstance(n, int) else n
-    z, y, x = np.meshgrid((np.arange(nz) + 0.5) / nz, (np.arange(ny) + 0.5) / ny,
-                          (np.arange(nx) + 0.5) / nx, indexing="ij")
-    if kind == "sphere_sinusoid":
-        r = np.sqrt((x - 0.5) ** 2 + (y - 0.5) ** 2 + (z - 0.5) ** 2)
-        shell = np.clip(1.0 - r / 0.45, 0.0, 1.0)
-        mod = 0.55 + 0.45 * np.sin(18.0 * x) * np.sin(18.0 * y) * np.sin(18.0 * z)
-        v = np.clip(shell * mod, 0.0, 1.0)
-    elif kind == "slab":
-        v = ((z >= 0.375) & (z <= 0.625)).astype(np.float64)
-    elif kind == "sphere":
-        r = np.sqrt((x - 0.5) ** 2 + (y - 0.5) ** 2 + (z - 0.5) ** 2)
-        v = (r <= 0.25).astype(np.float64)
-    elif kind.startswith("constant:"):
-        v = np.full(x.shape, float(kind.split(":")[1]))
-    else:
-        raise ValueError(f"unknown synthetic volume kind {kind!r}")
-    return np.ascontiguousarray(v.astype(np.float32))
+    out = np.empty((nz, ny, nx), dtype=np.float32)
+    y, x = np.meshgrid((np.arange(ny) + 0.5) / ny, (np.arange(nx) + 0.5) / nx, indexing="ij")
+    sx, sy = np.sin(18.0 * x), np.sin(18.0 * y)
+    for k in range(nz):  # slab by slab: bounded host memory even at 1024^3
+        z = (k + 0.5) / nz
+        if kind == "sphere_sinusoid":
+            r = np.sqrt((x - 0.5) ** 2 + (y - 0.5) ** 2 + (z - 0.5) ** 2)
+            shell = np.clip(1.0 - r / 0.45, 0.0, 1.0)
+            v = np.clip(shell * (0.55 + 0.45 * sx * sy * np.sin(18.0 * z)), 0.0, 1.0)
+        elif kind == "slab":
+            v = np.full(x.shape, 1.0 if 0.375 <= z <= 0.625 else 0.0)
+        elif kind == "sphere":
+            r = np.sqrt((x - 0.5) ** 2 + (y - 0.5) ** 2 + (z - 0.5) ** 2)
+            v = (r <= 0.25).astype(np.float64)
+        elif kind.startswith("constant:"):
+            v = np.full(x.shape, float(kind.split(":")[1]))
+        else:
+            raise ValueError(f"unknown synthetic volume kind {kind!r}")
+        out[k] = v
+    return out
 
 
 def validate_volume(v: np.ndarray) -> None:
