@@ -339,13 +339,16 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
             const int b = L & 1;
             const float *bl = bias + (L - 1) * 64;
 #pragma unroll
+            uint32_t acc[64];  // all four 16-column loads in flight, one wait
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld16(tmem_rows + 16 * c, acc + 16 * c);
+            tmem_ld_wait();
+            tmem_regs_ready<64>(acc);
+#pragma unroll
             for (int c = 0; c < 4; ++c) {
-                float v[16];
-                tmem_ld16(tmem_rows + 16 * c, v);
-                tmem_ld_wait();
                 float a[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) a[i] = fmaxf(v[i] + bl[16 * c + i], 0.f);
+                for (int i = 0; i < 16; ++i) a[i] = fmaxf(__uint_as_float(acc[16 * c + i]) + bl[16 * c + i], 0.f);
                 const uint32_t pa = buf_s[b] + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u;  // K=64: SBO 1024
                 store_feats<8>(pa, 0, 16 * c, 1024u, a);
                 store_feats<8>(pa, 0, 16 * c + 8, 1024u, a + 8);
@@ -364,10 +367,14 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
         }
 
         // ---- output layer epilogue: bias, Eq. 8 decode, compose term
-        float v[16];
-        tmem_ld16(tmem_rows, v);
+        uint32_t vr[16];
+        tmem_ld16(tmem_rows, vr);
         tmem_ld_wait();
+        tmem_regs_ready<16>(vr);
         tc_fence_before();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(vr[i]);
         named_bar_sync(1 + wg, 128);  // all rows read TMEM / A before the next tile reuses them
         const size_t row = tile * 128 + r, gr = P.row0 + row;
         if (row < n_items) {
