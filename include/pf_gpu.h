@@ -198,6 +198,35 @@ int pf_transmittance_ratio_batch(pf_ctx *ctx, size_t n, const double *a3, const 
 int pf_rng_doubles(pf_ctx *ctx, size_t n, uint64_t seed, uint64_t stream, const uint64_t *idx,
                    int n_draws, double *out);
 
+/* ---- photon tracing: Alg. 1 (photon.hpp:29-57) ---------- */
+/* pf::TraceConfig (photon.hpp:29-37). */
+typedef struct {
+    uint64_t n_total;         /* photons emitted, split over (light, phase) pairs */
+    int n_phases;             /* |G| (1..8) */
+    const double *phase_set;  /* G, distinct values in [-1, 1] */
+    int max_bounces;          /* default 16 */
+    int rr_start_bounce;      /* default 3 */
+    double rr_min_survival;   /* default 0.05 */
+    double rr_max_survival;   /* default 0.95 */
+    uint64_t seed;
+} pf_trace_desc;
+/* trace_photons(medium, lights, cfg) (photon.hpp:56; declared there, pinned in
+ * oracle/pf_oracle.c or_trace_photons): binary64 on the device over the
+ * context's medium + lights.  Photon i uses make_rng(seed, Trace, i), pair
+ * i % (nL*nG); records are in (photon index, bounce) order, identical to the
+ * oracle up to last-ulp libm differences.  The map stays resident in ctx;
+ * n_photons = deposits; emitted (optional, nL*nG) = TraceResult::emitted_per_pair.
+ * Zero lights / empty or invalid G -> PF_ERR_INVALID (std::invalid_argument). */
+int pf_trace_photons(pf_ctx *ctx, const pf_trace_desc *desc, size_t *n_photons, uint64_t *emitted);
+/* Copy the resident trace (n must equal n_photons) to host or device memory. */
+int pf_trace_fetch(pf_ctx *ctx, pf_photon *out, size_t n);
+/* Deposits per emitted photon (n_total entries), host or device memory. */
+int pf_trace_path_counts(pf_ctx *ctx, uint32_t *out, uint64_t n_total);
+/* Kernel times of the last trace (needs pf_ctx_set_timing) + tentative collisions. */
+int pf_trace_stats(pf_ctx *ctx, double *ms_trace, double *ms_compact, uint64_t *tentative_collisions);
+/* pf_knn_build straight from the resident trace (no host round trip). */
+int pf_knn_build_traced(pf_ctx *ctx, int n_phases, const double *phase_set);
+
 /* ---- photon map + KNN training-target gather (config 3) ----------------- */
 /* build(photons): per-phase cell grid, ids = load order. */
 int pf_knn_build(pf_ctx *ctx, const pf_photon *photons, size_t n, int n_phases,

@@ -73,6 +73,12 @@ class RenderCfg(C.Structure):
                 ("y1", C.c_int)]
 
 
+class TraceCfg(C.Structure):
+    _fields_ = [("n_total", C.c_uint64), ("n_phases", C.c_int), ("phase_set", C.c_void_p),
+                ("max_bounces", C.c_int), ("rr_start_bounce", C.c_int), ("rr_min_survival", C.c_double),
+                ("rr_max_survival", C.c_double), ("seed", C.c_uint64)]
+
+
 class RenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("hits", C.c_uint64)]
 
@@ -113,10 +119,17 @@ _SIG = {
                               _P, _P, _P, _P]),
     "or_camera_make": (None, [_P, _P, _P, _P, C.c_double, C.c_int, C.c_int]),
     "or_render_neural": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P]),
+    "or_hg_sample_cos": (C.c_double, [C.c_double, C.c_double]),
+    "or_hg_sample": (None, [C.c_double, _P, C.c_double, C.c_double, _P]),
+    "or_from_local_frame": (None, [_P, _P, _P]),
+    "or_emit_direction": (None, [_P, _P, _P]),
+    "or_trace_photons": (C.c_size_t, [_P, _P, C.c_int, _P, _P, C.c_size_t, _P, _P]),
 }
 
 _REF_SIG = {
     "ref_last_error": (C.c_char_p, []),
+    "ref_trace_photons": (C.c_size_t, [_P, _P, C.c_int, C.c_uint64, C.c_int, _P, C.c_int, C.c_int,
+                                       C.c_double, C.c_double, C.c_uint64, _P, _P, C.c_size_t]),
     "ref_rng_u32": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _P]),
     "ref_rng_double": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _P]),
     "ref_splitmix64": (C.c_uint64, [C.c_uint64]),
@@ -421,3 +434,66 @@ def ref_render_neural(scene: RefScene, lights, fc, params, cam_spec, rc, rect=No
                                _p(out), C.byref(hits)):
         raise ValueError(ref().ref_last_error().decode())
     return out, {"hits": hits.value}
+
+
+# ------------------------------------------------------- photon tracing --
+
+
+def hg_sample(g, w_in, u1, u2) -> np.ndarray:
+    w = np.ascontiguousarray(w_in, dtype=np.float64)
+    out = np.zeros(3)
+    lib().or_hg_sample(float(g), _p(w), float(u1), float(u2), _p(out))
+    return out
+
+
+def emit_directions(light_pos, seed, stream, idx) -> np.ndarray:
+    """emit_direction for photon streams make_rng(seed, stream, idx[i])."""
+    P = np.ascontiguousarray(light_pos, dtype=np.float64)
+    out = np.zeros((len(idx), 3))
+    st = (C.c_uint64 * 2)()
+    for i, j in enumerate(idx):
+        lib().or_make_rng(st, seed, stream, int(j))
+        lib().or_emit_direction(_p(P), st, _p(out[i]))
+    return out
+
+
+def trace_photons(scene: "OracleScene", lights, tc):
+    """trace_photons (Alg. 1) on the C restatement.
+
+    tc: object with n_total, phase_set, max_bounces, rr_start_bounce,
+    rr_min_survival, rr_max_survival, seed.  Returns (photons, emitted[pairs],
+    path_count[n_total]) with photons in the PHOTON_DTYPE layout (40 B)."""
+    from paper_2304_07338_b200.scene import PHOTON_DTYPE
+    gs = np.ascontiguousarray(tc.phase_set, dtype=np.float64)
+    cfg = TraceCfg(int(tc.n_total), len(gs), _p(gs), tc.max_bounces, tc.rr_start_bounce,
+                   float(tc.rr_min_survival), float(tc.rr_max_survival), int(tc.seed))
+    L = _lights(np.asarray(lights, dtype=np.float64))
+    emitted = np.zeros(max(1, len(lights) * len(gs)), np.uint64)
+    paths = np.zeros(max(1, int(tc.n_total)), np.int32)
+    cap = int(tc.n_total) * max(0, tc.max_bounces - 1) if tc.n_total < 200000 else int(tc.n_total) * 4
+    while True:
+        out = np.zeros(max(1, cap), dtype=PHOTON_DTYPE)
+        n = lib().or_trace_photons(C.byref(scene.medium), L, len(lights), C.byref(cfg), _p(out), cap,
+                                   _p(emitted), _p(paths))
+        if n <= cap:
+            break
+        cap = n
+    return out[:n].copy(), emitted[: len(lights) * len(gs)], paths[: int(tc.n_total)]
+
+
+def ref_trace_photons(scene: "RefScene", lights, tc):
+    """The pinned Alg. 1 composed from the reference's own primitives (ref_shim.cpp)."""
+    from paper_2304_07338_b200.scene import make_photons
+    L = np.ascontiguousarray(lights, dtype=np.float64).reshape(-1, 6)
+    gs = np.ascontiguousarray(tc.phase_set, dtype=np.float64)
+    cap = max(16, int(tc.n_total) * 4)
+    while True:
+        out9 = np.zeros((cap, 9), np.float32)
+        og = np.zeros(cap, np.uint8)
+        n = ref().ref_trace_photons(scene.h, _p(L), len(L), int(tc.n_total), len(gs), _p(gs),
+                                    tc.max_bounces, tc.rr_start_bounce, float(tc.rr_min_survival),
+                                    float(tc.rr_max_survival), int(tc.seed), _p(out9), _p(og), cap)
+        if n <= cap:
+            break
+        cap = n
+    return make_photons(out9[:n, 0:3], out9[:n, 3:6], out9[:n, 6:9], og[:n])

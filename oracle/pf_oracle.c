@@ -756,6 +756,122 @@ void or_knn_targets(const or_kdtree *t, const or_photon *ph, size_t nq, const fl
     }
 }
 
+/* ===== photon tracing: Alg. 1 ============================================= */
+
+/* hg_sample_cos, phase.hpp:26-31. */
+double or_hg_sample_cos(double g, double u) {
+    g = g < -0.999 ? -0.999 : (g > 0.999 ? 0.999 : g);
+    if (fabs(g) < 1e-6) return 1.0 - 2.0 * u;
+    double sq = (1.0 - g * g) / (1.0 - g + 2.0 * g * u);
+    double c = (1.0 + g * g - sq * sq) / (2.0 * g);
+    return c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+}
+
+/* orthonormal_basis (Duff et al.) + from_local_frame, math.hpp:113-126. */
+void or_from_local_frame(const double n[3], const double l[3], double out[3]) {
+    const double sign = copysign(1.0, n[2]);
+    const double a = -1.0 / (sign + n[2]);
+    const double c = n[0] * n[1] * a;
+    const double t[3] = {1.0 + sign * n[0] * n[0] * a, sign * c, -sign * n[0]};
+    const double b[3] = {c, sign + n[1] * n[1] * a, -n[1]};
+    for (int k = 0; k < 3; ++k) out[k] = t[k] * l[0] + b[k] * l[1] + n[k] * l[2];
+}
+
+/* hg_sample, phase.hpp:34-40. */
+void or_hg_sample(double g, const double w_in[3], double u1, double u2, double out[3]) {
+    double ct = or_hg_sample_cos(g, u1);
+    double t = 1.0 - ct * ct;
+    double st = sqrt(t > 0.0 ? t : 0.0);
+    double phi = OR_TWO_PI * u2;
+    double local[3] = {st * cos(phi), st * sin(phi), ct};
+    or_from_local_frame(w_in, local, out);
+}
+
+/* emit_direction (photon.hpp:50): uniform over the cone the
+ * unit box's bounding sphere (centre 0.5, radius sqrt(3)/2) subtends from the
+ * light; full sphere for lights inside it.  Pinned: cos = 1 - u1 (1 - cos_max),
+ * phi = 2 pi u2, rotated by from_local_frame about normalize(centre - P). */
+void or_emit_direction(const double P[3], or_pcg32 *rng, double out[3]) {
+    const double R = 0.5 * sqrt(3.0);
+    double v[3] = {0.5 - P[0], 0.5 - P[1], 0.5 - P[2]};
+    double d = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (d <= R) {
+        or_sample_uniform_sphere(rng, out);
+        return;
+    }
+    double axis[3] = {v[0] / d, v[1] / d, v[2] / d};
+    double s = R / d;
+    double t = 1.0 - s * s;
+    double cos_max = sqrt(t > 0.0 ? t : 0.0);
+    double u1 = or_next_double(rng), u2 = or_next_double(rng);
+    double ct = 1.0 - u1 * (1.0 - cos_max);
+    double t2 = 1.0 - ct * ct;
+    double st = sqrt(t2 > 0.0 ? t2 : 0.0);
+    double phi = OR_TWO_PI * u2;
+    double local[3] = {st * cos(phi), st * sin(phi), ct};
+    or_from_local_frame(axis, local, out);
+}
+
+/* trace_photons, pinned order:
+ *   for bounce = 0 .. max_bounces-1:
+ *     delta_track (miss -> stop); throughput *= alpha * rgb;
+ *     w = hg_sample(g, w, rng);  bounce >= 1 -> deposit {x, w (post-scatter),
+ *     I / n_pair * throughput, g_index};  bounce >= rr_start -> roulette with
+ *     q = clamp(max throughput, rr_min, rr_max): u >= q stops, else throughput /= q. */
+size_t or_trace_photons(const or_medium *m, const or_light *lights, int n_lights, const or_trace_cfg *cfg,
+                        or_photon *out, size_t capacity, uint64_t *emitted, int *path_count) {
+    const uint64_t pairs = (uint64_t)n_lights * (uint64_t)cfg->n_phases;
+    size_t n_out = 0;
+    if (pairs == 0) return 0;
+    for (uint64_t p = 0; p < pairs; ++p)
+        emitted[p] = cfg->n_total / pairs + (p < cfg->n_total % pairs ? 1u : 0u);
+    for (uint64_t i = 0; i < cfg->n_total; ++i) {
+        const uint64_t pr = i % pairs;
+        const int li = (int)(pr / (uint64_t)cfg->n_phases), gi = (int)(pr % (uint64_t)cfg->n_phases);
+        const double g = cfg->phase_set[gi];
+        or_pcg32 rng;
+        or_make_rng(&rng, cfg->seed, OR_STREAM_TRACE, i);
+        double o[3] = {lights[li].pos[0], lights[li].pos[1], lights[li].pos[2]}, w[3];
+        or_emit_direction(o, &rng, w);
+        double thr[3] = {1.0, 1.0, 1.0};
+        int deposited = 0;
+        for (int bounce = 0; bounce < cfg->max_bounces; ++bounce) {
+            double x[3], scal, c[4];
+            if (or_delta_track(m, o, w, 0.0, INFINITY, &rng, x, &scal, c) != 1) break;
+            for (int k = 0; k < 3; ++k) thr[k] *= c[3] * c[k];
+            double nw[3];
+            double u1 = or_next_double(&rng), u2 = or_next_double(&rng);
+            or_hg_sample(g, w, u1, u2, nw);
+            if (bounce >= 1) {
+                if (n_out < capacity) {
+                    or_photon *ph = &out[n_out];
+                    for (int k = 0; k < 3; ++k) {
+                        ph->pos[k] = (float)x[k];
+                        ph->dir[k] = (float)nw[k];
+                        ph->power[k] = (float)(lights[li].intensity[k] / (double)emitted[pr] * thr[k]);
+                    }
+                    ph->g_index = (uint8_t)gi;
+                }
+                ++n_out;
+                ++deposited;
+            }
+            if (bounce >= cfg->rr_start_bounce) {
+                double q = thr[0] > thr[1] ? thr[0] : thr[1];
+                q = thr[2] > q ? thr[2] : q;
+                q = q < cfg->rr_min_survival ? cfg->rr_min_survival : (q > cfg->rr_max_survival ? cfg->rr_max_survival : q);
+                if (or_next_double(&rng) >= q) break;
+                for (int k = 0; k < 3; ++k) thr[k] /= q;
+            }
+            for (int k = 0; k < 3; ++k) {
+                o[k] = x[k];
+                w[k] = nw[k];
+            }
+        }
+        if (path_count) path_count[i] = deposited;
+    }
+    return n_out;
+}
+
 /* ===== render_neural ====================================================== */
 
 static void or_normalize(double v[3]) {

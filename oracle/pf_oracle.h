@@ -180,6 +180,35 @@ void or_knn_targets(const or_kdtree *t, const or_photon *ph, size_t nq, const fl
                     float r_max, double psi, uint32_t *ids, float *d2, int *counts,
                     double *targets3);
 
+/* ---- photon tracing: Alg. 1, SPEC.md:151-219 ----------- */
+/* phase.hpp:26-46 + math.hpp:113-126 (checked bit-for-bit against the reference). */
+double or_hg_sample_cos(double g, double u);
+void or_hg_sample(double g, const double w_in[3], double u1, double u2, double out[3]);
+void or_from_local_frame(const double axis[3], const double local[3], double out[3]);
+
+typedef struct {
+    double pos[3];
+    double intensity[3];
+} or_light;
+
+typedef struct {
+    uint64_t n_total;
+    int n_phases;
+    const double *phase_set;
+    int max_bounces;
+    int rr_start_bounce;
+    double rr_min_survival, rr_max_survival;
+    uint64_t seed;
+} or_trace_cfg;
+
+/* emit_direction (photon.hpp:50, pinned in DESIGN.md). */
+void or_emit_direction(const double light_pos[3], or_pcg32 *rng, double out[3]);
+/* trace_photons: photon i -> pair p = i % (nL*nG), light p / nG, phase p % nG,
+ * rng = make_rng(seed, Trace, i); deposits in (i, bounce) order.  Returns the
+ * number of records (<= capacity); emitted[nL*nG]; path_count[i] optional. */
+size_t or_trace_photons(const or_medium *m, const or_light *lights, int n_lights, const or_trace_cfg *cfg,
+                        or_photon *out, size_t capacity, uint64_t *emitted, int *path_count);
+
 /* ---- render_neural (Alg. 2) ------------- */
 typedef struct {
     double origin[3];
@@ -195,11 +224,6 @@ void or_camera_make(or_camera *c, const double pos[3], const double look_at[3],
                     const double up[3], double vfov_deg, int width, int height);
 void or_camera_ray(const or_camera *c, int px, int py, double u, double v, double o[3],
                    double d[3]);
-
-typedef struct {
-    double pos[3];
-    double intensity[3];
-} or_light;
 
 typedef struct {
     int spp;

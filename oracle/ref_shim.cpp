@@ -8,6 +8,7 @@
 //       pf::delta_track / pf::transmittance driven by pf::parallel_chunks
 //       (proj/src/volume.cpp:204-256, proj/src/parallel.cpp:22-49); the
 //       SPEC-only field query / NEE glue / compose come from pf_oracle.c.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -110,6 +111,76 @@ void ref_tf_classify(void *h, double s, double rgba[4]) {
 
 // Batched pf::delta_track; ray i uses make_rng(seed, stream, idx[i]).
 // Returns 0, or 1 with ref_last_error() set if any ray is invalid.
+// trace_photons (photon.hpp:52-57) is declared by the reference but never
+// defined; this composes the pinned algorithm (see
+// pf_oracle.c or_trace_photons) from the reference's OWN primitives --
+// make_rng, Aabb::center/bounding_radius, sample_uniform_sphere,
+// from_local_frame, delta_track, hg_sample(g, w, rng) -- so the restatement's
+// composition is pinned against reference code, not against itself.
+// out: 10 floats + tag per deposit in (photon, bounce) order; returns count
+// (may exceed capacity, then only the first `capacity` are written).
+size_t ref_trace_photons(void *h, const double *lights, int n_lights, uint64_t n_total, int n_phases,
+                         const double *phase_set, int max_bounces, int rr_start, double rr_min, double rr_max,
+                         uint64_t seed, float *out9, uint8_t *out_g, size_t capacity) {
+    auto *s = static_cast<RefScene *>(h);
+    const pf::Aabb &box = s->medium->world_box();
+    const uint64_t pairs = (uint64_t)n_lights * (uint64_t)n_phases;
+    size_t n_out = 0;
+    for (uint64_t i = 0; i < n_total; ++i) {
+        const uint64_t pr = i % pairs;
+        const int li = (int)(pr / n_phases), gi = (int)(pr % n_phases);
+        const double n_pair = (double)(n_total / pairs + (pr < n_total % pairs ? 1u : 0u));
+        pf::Pcg32 rng = pf::make_rng(seed, pf::Stream::Trace, i);
+        const pf::Vec3 P{lights[6 * li], lights[6 * li + 1], lights[6 * li + 2]};
+        const pf::Vec3 I{lights[6 * li + 3], lights[6 * li + 4], lights[6 * li + 5]};
+        pf::Vec3 w;
+        {
+            const pf::Vec3 v = box.center() - P;
+            const double d = pf::length(v), R = box.bounding_radius();
+            if (d <= R) {
+                w = pf::sample_uniform_sphere(rng);
+            } else {
+                const pf::Vec3 axis = v / d;
+                const double sr = R / d;
+                const double cos_max = std::sqrt(std::max(0.0, 1.0 - sr * sr));
+                const double u1 = rng.next_double(), u2 = rng.next_double();
+                const double ct = 1.0 - u1 * (1.0 - cos_max);
+                const double st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
+                const double phi = pf::kTwoPi * u2;
+                w = pf::from_local_frame(axis, pf::Vec3{st * std::cos(phi), st * std::sin(phi), ct});
+            }
+        }
+        pf::Vec3 o = P, thr{1.0, 1.0, 1.0};
+        for (int bounce = 0; bounce < max_bounces; ++bounce) {
+            auto it = pf::delta_track(*s->medium, pf::Ray{o, w, 0.0, INFINITY}, rng);
+            if (!it) break;
+            thr = thr * pf::Vec3{it->albedo.a * it->albedo.r, it->albedo.a * it->albedo.g,
+                                 it->albedo.a * it->albedo.b};
+            const pf::Vec3 nw = pf::hg_sample(phase_set[gi], w, rng);
+            if (bounce >= 1) {
+                if (n_out < capacity) {
+                    float *r = out9 + 9 * n_out;
+                    for (int k = 0; k < 3; ++k) {
+                        r[k] = (float)it->position[k];
+                        r[3 + k] = (float)nw[k];
+                        r[6 + k] = (float)(I[k] / n_pair * thr[k]);
+                    }
+                    out_g[n_out] = (uint8_t)gi;
+                }
+                ++n_out;
+            }
+            if (bounce >= rr_start) {
+                const double q = std::clamp(std::max({thr.x, thr.y, thr.z}), rr_min, rr_max);
+                if (rng.next_double() >= q) break;
+                thr /= q;
+            }
+            o = it->position;
+            w = nw;
+        }
+    }
+    return n_out;
+}
+
 int ref_delta_track_batch(void *h, size_t n, const double *o3, const double *d3,
                           const double *tmin, const double *tmax, uint64_t seed, uint64_t stream,
                           const uint64_t *idx, int *hit, double *pos3, double *rgba4) {

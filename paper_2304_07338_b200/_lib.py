@@ -58,6 +58,14 @@ class Photon(C.Structure):
 
 assert C.sizeof(Photon) == 40
 
+
+class TraceDesc(C.Structure):
+    """pf::TraceConfig (proj/include/pf/photon.hpp:29-37)."""
+    _fields_ = [("n_total", C.c_uint64), ("n_phases", C.c_int), ("phase_set", C.c_void_p),
+                ("max_bounces", C.c_int), ("rr_start_bounce", C.c_int),
+                ("rr_min_survival", C.c_double), ("rr_max_survival", C.c_double),
+                ("seed", C.c_uint64)]
+
 _P = C.c_void_p
 _SIG = {
     "pf_last_error": (C.c_char_p, []),
@@ -90,6 +98,11 @@ _SIG = {
     "pf_transmittance_ratio_batch": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64,
                                                _P, C.c_int, _P]),
     "pf_rng_doubles": (C.c_int, [_P, C.c_size_t, C.c_uint64, C.c_uint64, _P, C.c_int, _P]),
+    "pf_trace_photons": (C.c_int, [_P, _P, _P, _P]),
+    "pf_trace_fetch": (C.c_int, [_P, _P, C.c_size_t]),
+    "pf_trace_stats": (C.c_int, [_P, _P, _P, _P]),
+    "pf_trace_path_counts": (C.c_int, [_P, _P, C.c_uint64]),
+    "pf_knn_build_traced": (C.c_int, [_P, C.c_int, _P]),
     "pf_knn_build": (C.c_int, [_P, _P, C.c_size_t, C.c_int, _P]),
     "pf_knn_query": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_int, C.c_float, _P, _P, _P]),
     "pf_knn_targets": (C.c_int, [_P, C.c_size_t, _P, _P, _P, C.c_int, C.c_float, C.c_double,

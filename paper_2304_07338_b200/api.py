@@ -5,6 +5,7 @@ Reference interface (namespace pf, /root/reference/proj + SPEC.md) -> here:
   pf::delta_track(medium, ray, rng)          Context.delta_track_batch
   pf::transmittance(medium, a, b, rng, n)    Context.transmittance_batch
   pf::make_rng(seed, stream, index)          Context.rng_doubles (device PCG32)
+  pf::trace_photons(medium, lights, cfg)     Context.trace_photons    (photon.hpp:56, Alg. 1)
   render_neural(scene, field, cfg, cam, spp) Context.render_neural   (SPEC.md:545)
   forward / infer_radiance                   Context.field_query
   build / knn_phase                          Context.knn_build / knn_query
@@ -104,6 +105,27 @@ class RenderConfig:
                                self.shard_index, self.shard_count)
 
 
+@dataclass
+class TraceConfig:
+    """pf::TraceConfig (proj/include/pf/photon.hpp:29-37)."""
+    n_total: int = 100000
+    phase_set: list = field(default_factory=lambda: [-0.75, 0.0, 0.75])
+    max_bounces: int = 16
+    rr_start_bounce: int = 3
+    rr_min_survival: float = 0.05
+    rr_max_survival: float = 0.95
+    seed: int = 0
+
+
+@dataclass
+class TraceResult:
+    """pf::TraceResult (photon.hpp:39-46)."""
+    photons: Any                 # PHOTON_DTYPE array (host) or uint8 CUDA tensor [n, 40]
+    phase_set: list
+    emitted_per_pair: np.ndarray  # index = light * |G| + phase
+    n_lights: int
+
+
 # ------------------------------------------------------------- helpers ----
 
 
@@ -147,6 +169,7 @@ class Context:
         self._h = h
         self.device = device
         self.field_config: FieldConfig | None = None
+        self.n_lights = 0
         if stream is not None:
             self.set_stream(stream)
 
@@ -199,6 +222,7 @@ class Context:
     def set_lights(self, lights) -> None:
         a = np.ascontiguousarray(lights, dtype=np.float64).reshape(-1, 6)
         check(lib().pf_lights_set(self._h, a.ctypes.data, a.shape[0]))
+        self.n_lights = a.shape[0]
 
     # ---- field
     def load_field(self, cfg: FieldConfig, params) -> None:
@@ -287,6 +311,44 @@ class Context:
         s = STREAM[stream] if isinstance(stream, str) else int(stream)
         check(lib().pf_rng_doubles(self._h, n, seed, s, pi, n_draws, po))
         return out
+
+    # ---- photon tracing (Alg. 1)
+    def trace_photons(self, tc: TraceConfig, device: bool = False) -> TraceResult:
+        """trace_photons on the device; photons come back to the host unless
+        device=True (then a uint8 CUDA tensor [n, 40] in the pf_photon layout)."""
+        gs = np.ascontiguousarray(tc.phase_set, dtype=np.float64)
+        d = _lib.TraceDesc(int(tc.n_total), len(gs), gs.ctypes.data, int(tc.max_bounces),
+                           int(tc.rr_start_bounce), float(tc.rr_min_survival),
+                           float(tc.rr_max_survival), int(tc.seed))
+        n_l = self.n_lights
+        emitted = np.zeros(max(1, n_l * len(gs)), np.uint64)
+        n = C.c_size_t(0)
+        check(lib().pf_trace_photons(self._h, C.byref(d), C.byref(n), emitted.ctypes.data))
+        n = n.value
+        if device:
+            import torch
+            out = torch.empty((n, 40), dtype=torch.uint8, device=f"cuda:{self.device}")
+            check(lib().pf_trace_fetch(self._h, out.data_ptr() if n else None, n))
+        else:
+            out = np.zeros(n, dtype=PHOTON_DTYPE)
+            check(lib().pf_trace_fetch(self._h, out.ctypes.data if n else None, n))
+        return TraceResult(out, list(gs), emitted[: n_l * len(gs)], n_l)
+
+    def trace_path_counts(self, n_total: int) -> np.ndarray:
+        out = np.zeros(max(1, n_total), np.uint32)
+        check(lib().pf_trace_path_counts(self._h, out.ctypes.data, n_total))
+        return out[:n_total]
+
+    def trace_stats(self) -> dict:
+        a, b, st = C.c_double(), C.c_double(), C.c_uint64()
+        check(lib().pf_trace_stats(self._h, C.byref(a), C.byref(b), C.byref(st)))
+        return {"ms_trace": a.value, "ms_compact": b.value, "tentative_collisions": st.value}
+
+    def knn_build_traced(self, phase_set) -> None:
+        """KNN build straight from the resident trace (no host round trip)."""
+        ps = np.ascontiguousarray(phase_set, dtype=np.float64)
+        check(lib().pf_knn_build_traced(self._h, len(ps), ps.ctypes.data))
+        self.phase_set = ps
 
     # ---- photon map / KNN
     def knn_build(self, photons, phase_set) -> None:

@@ -28,6 +28,7 @@ SOURCES = {
     "pf_field.cu": [],
     "pf_compose.cu": [],
     "pf_knn.cu": ["--fmad=false"],
+    "pf_photon.cu": ["--fmad=false"],
     "pf_capi.cu": [],
 }
 

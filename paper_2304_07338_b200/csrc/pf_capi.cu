@@ -22,6 +22,7 @@
 #include "pf_field.h"
 #include "pf_kernels.h"
 #include "pf_knn.h"
+#include "pf_photon.h"
 
 namespace pfk {
 cudaError_t launch_render_trace_parity(const DevScene &, const TraceParams &, int, cudaStream_t);
@@ -164,6 +165,12 @@ struct pf_ctx {
     KnnBuffers kb;
     DevBuf k_photons, k_bbox;
     size_t k_n = 0;
+    // photon trace (Alg. 1): resident result + scratch
+    DevBuf t_rec, t_rec_photon, t_counts, t_offs, t_tmp, t_out, t_ctr;
+    size_t t_n = 0;
+    unsigned long long trace_steps = 0;
+    uint64_t t_total = 0;
+    bool has_trace = false;
 
     cudaError_t stage_in(int slot, const void *host, size_t bytes, const void **dev) {
         if (!host || is_device_ptr(host)) {
@@ -940,6 +947,141 @@ int pf_rng_doubles(pf_ctx *c, size_t n, uint64_t seed, uint64_t stream, const ui
         PF_CUDA(cudaStreamSynchronize(c->stream));
     }
     return PF_OK;
+}
+
+// --------------------------------------------------------- photon trace --
+// Scratch deposits are 44 B each (record + owning photon); bound the first
+// attempt's scratch by this budget, retrace with the exact size on overflow.
+static constexpr size_t kTraceScratchBudget = size_t(4) << 30;
+
+int pf_trace_photons(pf_ctx *c, const pf_trace_desc *d, size_t *n_photons, uint64_t *emitted) {
+    if (!c || !d || (d->n_phases > 0 && !d->phase_set)) return set_err(PF_ERR_INVALID, "pf_trace_photons: null argument");
+    if (c->lights.empty()) return set_err(PF_ERR_INVALID, "TraceConfig: at least one light required");
+    if (d->n_phases < 1) return set_err(PF_ERR_INVALID, "TraceConfig: phase set must be non-empty");
+    if (d->n_phases > PF_MAX_TRACE_PHASES)
+        return set_err(PF_ERR_INVALID, "TraceConfig: at most %d phases", PF_MAX_TRACE_PHASES);
+    for (int g = 0; g < d->n_phases; ++g) {
+        if (!(d->phase_set[g] >= -1.0 && d->phase_set[g] <= 1.0))
+            return set_err(PF_ERR_INVALID, "TraceConfig: phase values must lie in [-1,1]");
+        for (int h = 0; h < g; ++h)
+            if (d->phase_set[h] == d->phase_set[g]) return set_err(PF_ERR_INVALID, "TraceConfig: phase values must be distinct");
+    }
+    if (d->max_bounces < 1) return set_err(PF_ERR_INVALID, "TraceConfig: max_bounces must be positive");
+    if (d->rr_start_bounce < 0) return set_err(PF_ERR_INVALID, "TraceConfig: rr_start_bounce must be >= 0");
+    if (!(d->rr_min_survival > 0.0 && d->rr_min_survival <= d->rr_max_survival && d->rr_max_survival <= 1.0))
+        return set_err(PF_ERR_INVALID, "TraceConfig: need 0 < rr_min_survival <= rr_max_survival <= 1");
+    if (d->n_total >= 0xFFFFFFFFull) return set_err(PF_ERR_INVALID, "TraceConfig: n_total must be < 2^32");
+    if (!c->vol_tex || !c->has_medium) return set_err(PF_ERR_INVALID, "pf_trace_photons: volume/medium not set");
+    PF_CUDA(cudaSetDevice(c->device));
+    const uint64_t n = d->n_total;
+    const uint64_t pairs = (uint64_t)(c->lights.size() / 6) * (uint64_t)d->n_phases;
+    if (emitted)
+        for (uint64_t p = 0; p < pairs; ++p) emitted[p] = n / pairs + (p < n % pairs ? 1u : 0u);
+    c->has_trace = false;
+    c->t_n = 0;
+    c->t_total = n;
+    if (n_photons) *n_photons = 0;
+    if (n == 0) {
+        c->has_trace = true;
+        return PF_OK;
+    }
+    PhotonTraceParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.n_total = n;
+    P.initstate = stream_initstate(d->seed, 1 /* Stream::Trace, rng.hpp:63 */);
+    P.n_phases = d->n_phases;
+    P.max_bounces = d->max_bounces;
+    P.rr_start = d->rr_start_bounce;
+    P.rr_min = d->rr_min_survival;
+    P.rr_max = d->rr_max_survival;
+    for (int g = 0; g < d->n_phases; ++g) P.g[g] = d->phase_set[g];
+    PF_CUDA(c->t_counts.ensure(n * 4));
+    PF_CUDA(c->t_ctr.ensure(16));
+    P.counts = (uint32_t *)c->t_counts.p;
+    P.counter = (unsigned long long *)c->t_ctr.p;
+    P.steps = P.counter + 1;
+    const uint64_t max_dep = n * (uint64_t)(d->max_bounces - 1);
+    uint64_t cap = std::min<uint64_t>(max_dep, std::max<uint64_t>(n * 4, 1024));
+    cap = std::min<uint64_t>(cap, kTraceScratchBudget / 44);
+    const DevScene S = c->scene();
+    unsigned long long hc[2] = {0, 0};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        PF_CUDA(c->t_rec.ensure(std::max<uint64_t>(cap, 1) * sizeof(PhotonOut)));
+        PF_CUDA(c->t_rec_photon.ensure(std::max<uint64_t>(cap, 1) * 4));
+        P.rec = (PhotonOut *)c->t_rec.p;
+        P.rec_photon = (uint32_t *)c->t_rec_photon.p;
+        P.cap = cap;
+        PF_CUDA(cudaMemsetAsync(c->t_ctr.p, 0, 16, c->stream));
+        if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+        PF_CUDA(launch_trace_photons(S, P, c->stream));
+        if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+        PF_CUDA(cudaMemcpyAsync(hc, c->t_ctr.p, 16, cudaMemcpyDeviceToHost, c->stream));
+        PF_CUDA(cudaStreamSynchronize(c->stream));
+        if (hc[0] <= cap) break;
+        cap = hc[0];  // deterministic: the retrace deposits exactly hc[0]
+    }
+    const uint64_t total = hc[0];
+    if (total >= 0xFFFFFFFFull) return set_err(PF_ERR_RUNTIME, "trace_photons: more than 2^32 deposits");
+    size_t tmp_bytes = 0;
+    PF_CUDA(photon_scan_bytes(n, &tmp_bytes));
+    PF_CUDA(c->t_tmp.ensure(tmp_bytes));
+    PF_CUDA(c->t_offs.ensure(n * 4));
+    PF_CUDA(c->t_out.ensure(std::max<uint64_t>(total, 1) * sizeof(PhotonOut)));
+    if (c->timing) cudaEventRecord(c->ev[3], c->stream);
+    PF_CUDA(launch_photon_compact(P.counts, (uint32_t *)c->t_offs.p, n, c->t_tmp.p, tmp_bytes, P.rec,
+                                  P.rec_photon, total, (PhotonOut *)c->t_out.p, c->stream));
+    if (c->timing) cudaEventRecord(c->ev[2], c->stream);
+    c->t_n = total;
+    c->trace_steps = hc[1];
+    c->has_trace = true;
+    if (n_photons) *n_photons = total;
+    return PF_OK;
+}
+
+int pf_trace_fetch(pf_ctx *c, pf_photon *out, size_t n) {
+    if (!c || (n && !out)) return set_err(PF_ERR_INVALID, "pf_trace_fetch: null argument");
+    if (!c->has_trace) return set_err(PF_ERR_INVALID, "pf_trace_fetch: call pf_trace_photons first");
+    if (n != c->t_n) return set_err(PF_ERR_INVALID, "pf_trace_fetch: expected %zu records", c->t_n);
+    if (n == 0) return PF_OK;
+    PF_CUDA(cudaSetDevice(c->device));
+    const bool dev = is_device_ptr(out);
+    PF_CUDA(cudaMemcpyAsync(out, c->t_out.p, n * sizeof(pf_photon),
+                            dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    if (!dev) PF_CUDA(cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+int pf_trace_path_counts(pf_ctx *c, uint32_t *out, uint64_t n_total) {
+    if (!c || (n_total && !out)) return set_err(PF_ERR_INVALID, "pf_trace_path_counts: null argument");
+    if (!c->has_trace) return set_err(PF_ERR_INVALID, "pf_trace_path_counts: call pf_trace_photons first");
+    if (n_total != c->t_total) return set_err(PF_ERR_INVALID, "pf_trace_path_counts: expected %llu photons",
+                                              (unsigned long long)c->t_total);
+    if (n_total == 0) return PF_OK;
+    PF_CUDA(cudaSetDevice(c->device));
+    const bool dev = is_device_ptr(out);
+    PF_CUDA(cudaMemcpyAsync(out, c->t_counts.p, n_total * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            c->stream));
+    if (!dev) PF_CUDA(cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+int pf_trace_stats(pf_ctx *c, double *ms_trace, double *ms_compact, uint64_t *tentative_collisions) {
+    if (!c || !c->has_trace) return set_err(PF_ERR_INVALID, "pf_trace_stats: call pf_trace_photons first");
+    if (tentative_collisions) *tentative_collisions = c->trace_steps;
+    float a = 0.f, b = 0.f;
+    if (c->timing && c->t_n > 0) {
+        PF_CUDA(cudaEventSynchronize(c->ev[2]));
+        PF_CUDA(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
+        PF_CUDA(cudaEventElapsedTime(&b, c->ev[3], c->ev[2]));
+    }
+    if (ms_trace) *ms_trace = a;
+    if (ms_compact) *ms_compact = b;
+    return PF_OK;
+}
+
+int pf_knn_build_traced(pf_ctx *c, int n_phases, const double *phase_set) {
+    if (!c || !c->has_trace) return set_err(PF_ERR_INVALID, "pf_knn_build_traced: call pf_trace_photons first");
+    return pf_knn_build(c, (const pf_photon *)c->t_out.p, c->t_n, n_phases, phase_set);
 }
 
 // ------------------------------------------------------------------ knn --
