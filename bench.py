@@ -438,6 +438,27 @@ def bench_extras(ctx, fc, params, peaks, rank=0, world=1):
                                        "frac": qps * flop / 1e12 / (float(peaks["bf16_tflops"]) * world)},
                           "gather_bytes_per_query": 2 * (fc.pos.levels * 8 * fc.pos.features +
                                                          fc.dir.levels * 4 * fc.dir.features)}
+    # f1: photon tracing (Alg. 1) of 1M photons through this scene, binary64
+    # (the paper's smallest map: 4.2-23.8 s on 2x Xeon)
+    from paper_2304_07338_b200.api import TraceConfig
+    tc = TraceConfig(n_total=1_000_000, seed=3)
+    ctx.set_timing(True)
+    for _ in range(2):
+        tr = ctx.trace_photons(tc, device=True)
+    ts = [], []
+    for _ in range(3):
+        tr = ctx.trace_photons(tc, device=True)
+        st = ctx.trace_stats()
+        ts[0].append(st["ms_trace"])
+        ts[1].append(st["ms_compact"])
+    ctx.set_timing(False)
+    ms = float(np.median(ts[0])) + float(np.median(ts[1]))
+    out["photon_trace"] = {"photons_per_s": _sum_over_ranks(tc.n_total / (ms / 1e3), world),
+                           "n_photons": tc.n_total, "deposits": int(tr.photons.shape[0]),
+                           "ms_trace": float(np.median(ts[0])), "ms_compact": float(np.median(ts[1])),
+                           "tentative_collisions": st["tentative_collisions"], "precision": "f64",
+                           "ranks": world, "scaling": "weak"}
+    del tr
     # config 3: KNN radiance estimate (k = 64) over a 4M-photon 3-phase map,
     # 2^20 device-resident queries per batch, CUDA-event timed
     sys.path.insert(0, str(ROOT / "tools"))

@@ -70,6 +70,7 @@ class Device {
             v.insert(v.end(), {l.position.x, l.position.y, l.position.z, l.intensity.x, l.intensity.y,
                                l.intensity.z});
         check(pf_lights_set(ctx_, v.data(), (int)lights.size()));
+        n_lights_ = lights.size();
     }
 
     // Batched pf::delta_track (volume.cpp:204-225).
@@ -136,6 +137,24 @@ class Device {
         return frame;
     }
 
+    // trace_photons(medium, lights, cfg) (photon.hpp:56 -- declared by the
+    // reference, defined here on the device): call set_medium / set_lights
+    // first.  Returns the reference's TraceResult with the photons in
+    // (photon index, bounce) order and emitted_per_pair filled.
+    pf::TraceResult trace_photons(const pf::TraceConfig &cfg) {
+        pf_trace_desc d{cfg.n_total, (int)cfg.phase_set.size(), cfg.phase_set.data(), cfg.max_bounces,
+                        cfg.rr_start_bounce, cfg.rr_min_survival, cfg.rr_max_survival, cfg.seed};
+        pf::TraceResult r;
+        r.phase_set = cfg.phase_set;
+        r.n_lights = n_lights_;
+        r.emitted_per_pair.resize(n_lights_ * cfg.phase_set.size());
+        size_t n = 0;
+        check(pf_trace_photons(ctx_, &d, &n, r.emitted_per_pair.data()));
+        r.photons.resize(n);
+        check(pf_trace_fetch(ctx_, reinterpret_cast<pf_photon *>(r.photons.data()), n));
+        return r;
+    }
+
     // build(photons) -- ids are load-order indices into `photons`.
     void build(const std::vector<pf::Photon> &photons, const std::vector<double> &phase_set) {
         check(pf_knn_build(ctx_, reinterpret_cast<const pf_photon *>(photons.data()), photons.size(),
@@ -160,6 +179,7 @@ class Device {
     pf_ctx *ctx_ = nullptr;
     int nx_ = 0, ny_ = 0, nz_ = 0;
     const float *vol_ = nullptr;
+    size_t n_lights_ = 0;
 };
 
 }  // namespace pf::gpu

@@ -18,7 +18,12 @@ int main() {
         auto its = dev.delta_track(rays, 7, pf::Stream::CameraSample, {0, 1, 2, 3});
         int hits = 0;
         for (auto &it : its) hits += it.has_value();
-        std::printf("gpu ok hits=%d\n", hits);
+        dev.set_lights({pf::LightSource{{2.0, 2.5, -1.0}, {1.0, 1.0, 1.0}}});
+        pf::TraceConfig tc;
+        tc.n_total = 1000;
+        pf::TraceResult tr = dev.trace_photons(tc);
+        if (tr.emitted_per_pair.size() != 3 || tr.photons.empty()) return 4;
+        std::printf("gpu ok hits=%d photons=%zu\n", hits, tr.photons.size());
         try {
             dev.transmittance({{0, 0, 0}}, {{1, 1, 1}}, 0, pf::Stream::Nee, {0}, 0);
             return 3;
