@@ -137,6 +137,23 @@ class Device {
         return frame;
     }
 
+    // render_path_traced: NEE + HG continuation + roulette.
+    std::vector<float> render_path_traced(const pf_camera &cam, const pf_render_desc &desc,
+                                          const pf_path_desc &path, pf_render_stats *stats = nullptr) {
+        std::vector<float> frame((size_t)cam.width * cam.height * 3, 0.0f);
+        check(pf_render_path_traced(ctx_, &cam, &desc, &path, frame.data(), stats));
+        return frame;
+    }
+
+    // render_photon_map: L_i = Eq. 6 over the resident map;
+    // desc.g outside the map's phase set throws std::invalid_argument.
+    std::vector<float> render_photon_map(const pf_camera &cam, const pf_render_desc &desc, int K, float r_max,
+                                         pf_render_stats *stats = nullptr) {
+        std::vector<float> frame((size_t)cam.width * cam.height * 3, 0.0f);
+        check(pf_render_photon_map(ctx_, &cam, &desc, K, r_max, frame.data(), stats));
+        return frame;
+    }
+
     // trace_photons(medium, lights, cfg) (photon.hpp:56 -- declared by the
     // reference, defined here on the device): call set_medium / set_lights
     // first.  Returns the reference's TraceResult with the photons in

@@ -168,6 +168,30 @@ int pf_camera_make(const double pos[3], const double look_at[3], const double up
  * pixels of other shards are left untouched.  stats may be NULL. */
 int pf_render_neural(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
                      float *out_rgb, pf_render_stats *stats);
+/* ---- the comparison renderers of SPEC.md render module ------------------ */
+/* render_path_traced(scene, camera, spp, max_bounces, rng):
+ * the volumetric path tracer with NEE at every vertex, HG-sampled
+ * continuation and Russian roulette (pinned: oracle or_render_path_traced).
+ * Identical to pf_render_neural up to the first interaction's NEE (same
+ * CameraSample / Nee streams); the continuation runs on make_rng(seed,
+ * PathTrace, index).  desc->use_field is ignored. */
+typedef struct {
+    int max_bounces;         /* path vertices incl. the first interaction, >= 1 (16) */
+    int rr_start_bounce;     /* roulette from this vertex on (3) */
+    double rr_min_survival;  /* 0.05 */
+    double rr_max_survival;  /* 0.95 */
+} pf_path_desc;
+int pf_render_path_traced(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
+                          const pf_path_desc *path, float *out_rgb, pf_render_stats *stats);
+/* render_photon_map(scene, map, camera, spp, K, r_max, g, rng):
+ * render_neural with L_i = Eq. 6 over knn_phase of the resident photon map
+ * (pf_knn_build / pf_knn_build_traced) at each first interaction (query =
+ * position as binary32, omega = -ray direction).  desc->g must be one of the
+ * map's phase values (else PF_ERR_INVALID, "g not in the map's phase set");
+ * K in [1, 1024], r_max > 0.  desc->use_field is ignored. */
+int pf_render_photon_map(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc, int K,
+                         float r_max, float *out_rgb, pf_render_stats *stats);
+
 /* Multi-GPU helpers: pack this shard's tiles contiguously (tile order) and
  * unpack all shards' packed buffers into a frame. */
 int pf_tiles_count(const pf_camera *cam, const pf_render_desc *desc, int shard, int *n_tiles);

@@ -83,6 +83,16 @@ class RenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("hits", C.c_uint64)]
 
 
+class PtCfg(C.Structure):
+    _fields_ = [("max_bounces", C.c_int), ("rr_start_bounce", C.c_int), ("rr_min_survival", C.c_double),
+                ("rr_max_survival", C.c_double)]
+
+
+class PmSrc(C.Structure):
+    _fields_ = [("ph", C.c_void_p), ("n", C.c_size_t), ("tree", C.c_void_p), ("g_index", C.c_int),
+                ("K", C.c_int), ("r_max", C.c_float)]
+
+
 _P = C.c_void_p
 _SIG = {
     "or_next_u32": (C.c_uint32, [_P]),
@@ -119,6 +129,8 @@ _SIG = {
                               _P, _P, _P, _P]),
     "or_camera_make": (None, [_P, _P, _P, _P, C.c_double, C.c_int, C.c_int]),
     "or_render_neural": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P]),
+    "or_render_path_traced": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P]),
+    "or_render_photon_map": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P]),
     "or_hg_sample_cos": (C.c_double, [C.c_double, C.c_double]),
     "or_hg_sample": (None, [C.c_double, _P, C.c_double, C.c_double, _P]),
     "or_from_local_frame": (None, [_P, _P, _P]),
@@ -149,6 +161,7 @@ _REF_SIG = {
     "ref_transmittance_batch": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64, _P,
                                           C.c_int, _P]),
     "ref_render_neural": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P]),
+    "ref_render_path_traced": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P]),
 }
 
 _lib = None
@@ -434,6 +447,52 @@ def ref_render_neural(scene: RefScene, lights, fc, params, cam_spec, rc, rect=No
                                _p(out), C.byref(hits)):
         raise ValueError(ref().ref_last_error().decode())
     return out, {"hits": hits.value}
+
+
+def _ptcfg(pt) -> PtCfg:
+    return PtCfg(int(pt.max_bounces), int(pt.rr_start_bounce), float(pt.rr_min_survival),
+                 float(pt.rr_max_survival))
+
+
+def render_path_traced(scene: OracleScene, lights, cam_spec, rc, pt, rect=None):
+    """render_path_traced on the C restatement: render_neural's
+    first interaction + NEE, L_i from a phase-sampled continuation (PathTrace stream)."""
+    cam = camera(cam_spec)
+    ls = _lights(np.asarray(lights, np.float64).reshape(-1, 6))
+    out = np.zeros((cam.height, cam.width, 3), np.float32)
+    st = RenderStats()
+    lib().or_render_path_traced(C.byref(scene.medium), ls, len(ls), C.byref(cam), C.byref(_rcfg(rc, cam, rect)),
+                                C.byref(_ptcfg(pt)), _p(out), C.byref(st))
+    return out, {"samples": st.samples, "hits": st.hits}
+
+
+def ref_render_path_traced(scene: "RefScene", lights, cam_spec, rc, pt, rect=None, workers=0):
+    """The same algorithm composed from the reference's own primitives (ref_shim.cpp)."""
+    cam = camera(cam_spec)
+    ls = _lights(np.asarray(lights, np.float64).reshape(-1, 6))
+    out = np.zeros((cam.height, cam.width, 3), np.float32)
+    hits = C.c_uint64()
+    if ref().ref_render_path_traced(scene.h, ls, len(ls), C.byref(cam), C.byref(_rcfg(rc, cam, rect)),
+                                    C.byref(_ptcfg(pt)), workers or (os.cpu_count() or 1), _p(out),
+                                    C.byref(hits)):
+        raise ValueError(ref().ref_last_error().decode())
+    return out, {"hits": hits.value}
+
+
+def render_photon_map(scene: OracleScene, lights, photons, g_index, K, r_max, cam_spec, rc, rect=None,
+                      tree: "KdTree | None" = None):
+    """render_photon_map on the C restatement: L_i = Eq. 6 over
+    knn_phase(x as binary32, g_index, K, r_max) at the first interaction."""
+    cam = camera(cam_spec)
+    ls = _lights(np.asarray(lights, np.float64).reshape(-1, 6))
+    ph = tree.ph if tree is not None else np.ascontiguousarray(photons)
+    src = PmSrc(_p(ph) if len(ph) else None, len(ph), tree.t if tree is not None else None, int(g_index),
+                int(K), float(r_max))
+    out = np.zeros((cam.height, cam.width, 3), np.float32)
+    st = RenderStats()
+    lib().or_render_photon_map(C.byref(scene.medium), ls, len(ls), C.byref(src), C.byref(cam),
+                               C.byref(_rcfg(rc, cam, rect)), _p(out), C.byref(st))
+    return out, {"samples": st.samples, "hits": st.hits}
 
 
 # ------------------------------------------------------- photon tracing --

@@ -933,9 +933,76 @@ void or_shade_sample(const double Ld[3], const double Li[3], const double rgba[4
     for (int ch = 0; ch < 3; ++ch) out[ch] = w_d * Ld[ch] + w_i * (sigma_s * Li[ch]);
 }
 
-void or_render_neural(const or_medium *m, const or_light *lights, int n_lights,
-                      const or_field_cfg *fc, const float *params, const or_camera *cam,
-                      const or_render_cfg *rc, float *out_rgb, or_render_stats *st) {
+/* render_path_traced's continuation (pinned in DESIGN.md):
+ * the in-scattered radiance L_i at the first interaction x0, estimated by a
+ * phase-sampled path on make_rng(seed, PathTrace, index).  Vertex k >= 1:
+ *   w = hg_sample(g, w, rng); x_k = delta_track(x_{k-1}, w) (miss -> stop);
+ *   L_d(x_k) = sum_l nee_term(x_k, -w, l, g, transmittance(x_k, P_l, rng, trials));
+ *   L_i += thr * L_d(x_k); thr *= sigma_s(x_k) (stop at 0);
+ *   k >= rr_start: q = clamp(thr, rr_min, rr_max), next_double() >= q stops, else thr /= q.
+ * Point lights cannot be hit by phase sampling, so the balance-heuristic MIS
+ * weight of NEE is 1 and escaped continuations carry no radiance. */
+static void or_pt_indirect(const or_medium *m, const or_light *lights, int n_lights,
+                           const or_render_cfg *rc, const or_pt_cfg *pt, uint64_t index,
+                           const double x0[3], const double d0[3], double Li[3]) {
+    Li[0] = Li[1] = Li[2] = 0.0;
+    if (pt->max_bounces <= 1) return;
+    or_pcg32 r;
+    or_make_rng(&r, rc->seed, OR_STREAM_PATHTRACE, index);
+    double o[3] = {x0[0], x0[1], x0[2]}, w[3] = {d0[0], d0[1], d0[2]};
+    double thr = 1.0;
+    for (int k = 1; k < pt->max_bounces; ++k) {
+        double u1 = or_next_double(&r), u2 = or_next_double(&r), nw[3];
+        or_hg_sample(rc->g, w, u1, u2, nw);
+        w[0] = nw[0];
+        w[1] = nw[1];
+        w[2] = nw[2];
+        double x[3], scal, rgba[4];
+        if (or_delta_track(m, o, w, 0.0, INFINITY, &r, x, &scal, rgba) != 1) break;
+        double w_out[3] = {-w[0], -w[1], -w[2]};
+        double Ld[3] = {0.0, 0.0, 0.0};
+        for (int l = 0; l < n_lights; ++l) {
+            double T = or_transmittance(m, x, lights[l].pos, &r, rc->nee_trials);
+            or_nee_term(x, w_out, &lights[l], rc->g, T, Ld);
+        }
+        for (int ch = 0; ch < 3; ++ch) Li[ch] += thr * Ld[ch];
+        thr *= rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / 3.0);
+        if (!(thr > 0.0)) break;
+        if (k >= pt->rr_start_bounce) {
+            double q = thr < pt->rr_min_survival ? pt->rr_min_survival
+                                                  : (thr > pt->rr_max_survival ? pt->rr_max_survival : thr);
+            if (or_next_double(&r) >= q) break;
+            thr /= q;
+        }
+        o[0] = x[0];
+        o[1] = x[1];
+        o[2] = x[2];
+    }
+}
+
+/* render_photon_map's L_i: Eq. 6 over knn_phase at the
+ * first interaction, query position rounded to binary32 (App. B.8), omega =
+ * w_out in binary64, g = the map's phase value. */
+static void or_pm_radiance(const or_pm_src *pm, const double x[3], const double w_out[3], double g,
+                           double Li[3]) {
+    Li[0] = Li[1] = Li[2] = 0.0;
+    if (pm->K <= 0) return;
+    uint32_t ids[1024];
+    float d2[1024];
+    const float q[3] = {(float)x[0], (float)x[1], (float)x[2]};
+    int c = pm->tree ? or_kd_knn(pm->tree, q, pm->g_index, pm->K, pm->r_max, ids, d2)
+                     : or_knn_brute(pm->ph, pm->n, q, pm->g_index, pm->K, pm->r_max, ids, d2);
+    or_estimate_radiance(pm->ph, ids, d2, c, w_out, g, Li);
+}
+
+/* The shared per-sample program of the three first-interaction renderers:
+ * camera jitter + delta_track on CameraSample, NEE on the Nee stream, then
+ * L_i from the field (neural), a continued path (path traced) or the photon
+ * map, composed as w_d L_d + w_i sigma_s L_i. */
+static void or_render_impl(const or_medium *m, const or_light *lights, int n_lights,
+                           const or_camera *cam, const or_render_cfg *rc, const or_field_cfg *fc,
+                           const float *params, const or_pt_cfg *pt, const or_pm_src *pm,
+                           float *out_rgb, or_render_stats *st) {
     const int W = cam->width, spp = rc->spp;
     for (int py = rc->y0; py < rc->y1; ++py) {
         for (int px = rc->x0; px < rc->x1; ++px) {
@@ -963,7 +1030,11 @@ void or_render_neural(const or_medium *m, const or_light *lights, int n_lights,
                         double T = or_transmittance(m, x, lights[l].pos, &nee, rc->nee_trials);
                         or_nee_term(x, w_out, &lights[l], rc->g, T, Ld);
                     }
-                    if (rc->use_field) {
+                    if (pt) {
+                        or_pt_indirect(m, lights, n_lights, rc, pt, index, x, d, Li);
+                    } else if (pm) {
+                        or_pm_radiance(pm, x, w_out, rc->g, Li);
+                    } else if (rc->use_field) {
                         double sph[2];
                         or_dir_to_sph(w_out, sph);
                         or_field_infer(fc, params, 1, x, sph, &rc->g, Li);
@@ -976,4 +1047,22 @@ void or_render_neural(const or_medium *m, const or_light *lights, int n_lights,
             for (int ch = 0; ch < 3; ++ch) o3[ch] = (float)(acc[ch] / (double)spp);
         }
     }
+}
+
+void or_render_neural(const or_medium *m, const or_light *lights, int n_lights,
+                      const or_field_cfg *fc, const float *params, const or_camera *cam,
+                      const or_render_cfg *rc, float *out_rgb, or_render_stats *st) {
+    or_render_impl(m, lights, n_lights, cam, rc, fc, params, NULL, NULL, out_rgb, st);
+}
+
+void or_render_path_traced(const or_medium *m, const or_light *lights, int n_lights,
+                           const or_camera *cam, const or_render_cfg *rc, const or_pt_cfg *pt,
+                           float *out_rgb, or_render_stats *st) {
+    or_render_impl(m, lights, n_lights, cam, rc, NULL, NULL, pt, NULL, out_rgb, st);
+}
+
+void or_render_photon_map(const or_medium *m, const or_light *lights, int n_lights,
+                          const or_pm_src *pm, const or_camera *cam, const or_render_cfg *rc,
+                          float *out_rgb, or_render_stats *st) {
+    or_render_impl(m, lights, n_lights, cam, rc, NULL, NULL, NULL, pm, out_rgb, st);
 }

@@ -251,6 +251,32 @@ void or_render_neural(const or_medium *m, const or_light *lights, int n_lights,
                       const or_field_cfg *fc, const float *params, const or_camera *cam,
                       const or_render_cfg *rc, float *out_rgb, or_render_stats *st);
 
+/* ---- render_path_traced -------------------------------- */
+typedef struct {
+    int max_bounces;      /* path vertices incl. the first interaction (default 16) */
+    int rr_start_bounce;  /* roulette from this vertex on (default 3) */
+    double rr_min_survival, rr_max_survival; /* 0.05, 0.95 */
+} or_pt_cfg;
+/* Identical to render_neural up to and including the first interaction's NEE
+ * (same CameraSample / Nee streams); L_i from a phase-sampled continuation on
+ * make_rng(seed, PathTrace, index) (pinned in pf_oracle.c or_pt_indirect). */
+void or_render_path_traced(const or_medium *m, const or_light *lights, int n_lights,
+                           const or_camera *cam, const or_render_cfg *rc, const or_pt_cfg *pt,
+                           float *out_rgb, or_render_stats *st);
+
+/* ---- render_photon_map --------------------------------- */
+typedef struct {
+    const or_photon *ph;
+    size_t n;
+    const or_kdtree *tree; /* NULL: brute force */
+    int g_index;           /* the render g's index in the map's phase set */
+    int K;                 /* <= 1024 */
+    float r_max;
+} or_pm_src;
+void or_render_photon_map(const or_medium *m, const or_light *lights, int n_lights,
+                          const or_pm_src *pm, const or_camera *cam, const or_render_cfg *rc,
+                          float *out_rgb, or_render_stats *st);
+
 #ifdef __cplusplus
 }
 #endif

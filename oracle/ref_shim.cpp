@@ -296,4 +296,91 @@ int ref_render_neural(void *h, const or_light *lights, int n_lights, const or_fi
     return 0;
 }
 
+// render_path_traced composed from the reference's OWN
+// primitives -- make_rng, delta_track, transmittance, hg_sample(g, w, rng) --
+// with the order pinned in pf_oracle.c or_render_path_traced / or_pt_indirect,
+// driven by the reference's parallel_chunks.  Rows [y0, y1) into out_rgb.
+int ref_render_path_traced(void *h, const or_light *lights, int n_lights, const or_camera *cam,
+                           const or_render_cfg *rc, const or_pt_cfg *pt, int workers, float *out_rgb,
+                           uint64_t *hits_out) {
+    auto *s = static_cast<RefScene *>(h);
+    const int W = cam->width, spp = rc->spp;
+    pf::set_worker_count(workers);
+    const size_t npix = (size_t)(rc->y1 - rc->y0) * (size_t)(rc->x1 - rc->x0);
+    std::vector<uint64_t> chunk_hits((npix + 63) / 64, 0);
+    auto lit = [&](const pf::Vec3 &x, const double w_out[3], pf::Pcg32 &rng, double Ld[3]) {
+        const double xa[3] = {x.x, x.y, x.z};
+        for (int l = 0; l < n_lights; ++l) {
+            const double T = pf::transmittance(*s->medium, x, {lights[l].pos[0], lights[l].pos[1], lights[l].pos[2]},
+                                               rng, rc->nee_trials);
+            or_nee_term(xa, w_out, &lights[l], rc->g, T, Ld);
+        }
+    };
+    try {
+        pf::parallel_chunks(npix, 64, [&](size_t ci, size_t b, size_t e) {
+            uint64_t hits = 0;
+            for (size_t p = b; p < e; ++p) {
+                const int px = rc->x0 + (int)(p % (size_t)(rc->x1 - rc->x0));
+                const int py = rc->y0 + (int)(p / (size_t)(rc->x1 - rc->x0));
+                double acc[3] = {0.0, 0.0, 0.0};
+                for (int k = 0; k < spp; ++k) {
+                    const uint64_t index = ((uint64_t)py * (uint64_t)W + (uint64_t)px) * (uint64_t)spp + k;
+                    pf::Pcg32 rng = pf::make_rng(rc->seed, pf::Stream::CameraSample, index);
+                    const double u = rng.next_double();
+                    const double v = rng.next_double();
+                    double o[3], d[3];
+                    or_camera_ray(cam, px, py, u, v, o, d);
+                    auto it = pf::delta_track(*s->medium, pf::Ray{{o[0], o[1], o[2]}, {d[0], d[1], d[2]}, 0.0,
+                                                                  pf::kInfinity},
+                                              rng);
+                    double sample[3];
+                    if (!it) {
+                        for (int c = 0; c < 3; ++c) sample[c] = rc->background[c];
+                    } else {
+                        ++hits;
+                        const double w_out[3] = {-d[0], -d[1], -d[2]};
+                        double Ld[3] = {0, 0, 0}, Li[3] = {0, 0, 0};
+                        pf::Pcg32 nee = pf::make_rng(rc->seed, pf::Stream::Nee, index);
+                        lit(it->position, w_out, nee, Ld);
+                        if (pt->max_bounces > 1) {
+                            pf::Pcg32 r = pf::make_rng(rc->seed, pf::Stream::PathTrace, index);
+                            pf::Vec3 x = it->position, w{d[0], d[1], d[2]};
+                            double thr = 1.0;
+                            for (int b2 = 1; b2 < pt->max_bounces; ++b2) {
+                                w = pf::hg_sample(rc->g, w, r);
+                                auto nx = pf::delta_track(*s->medium, pf::Ray{x, w, 0.0, pf::kInfinity}, r);
+                                if (!nx) break;
+                                const double wo[3] = {-w.x, -w.y, -w.z};
+                                double Lk[3] = {0, 0, 0};
+                                lit(nx->position, wo, r, Lk);
+                                for (int c = 0; c < 3; ++c) Li[c] += thr * Lk[c];
+                                thr *= nx->albedo.a * ((nx->albedo.r + nx->albedo.g + nx->albedo.b) / 3.0);
+                                if (!(thr > 0.0)) break;
+                                if (b2 >= pt->rr_start_bounce) {
+                                    const double q = std::clamp(thr, pt->rr_min_survival, pt->rr_max_survival);
+                                    if (r.next_double() >= q) break;
+                                    thr /= q;
+                                }
+                                x = nx->position;
+                            }
+                        }
+                        const double rgba[4] = {it->albedo.r, it->albedo.g, it->albedo.b, it->albedo.a};
+                        or_shade_sample(Ld, Li, rgba, rc->w_d, rc->w_i, sample);
+                    }
+                    for (int c = 0; c < 3; ++c) acc[c] += sample[c];
+                }
+                float *o3 = out_rgb + 3 * ((size_t)py * W + px);
+                for (int c = 0; c < 3; ++c) o3[c] = (float)(acc[c] / (double)spp);
+            }
+            chunk_hits[ci] = hits;
+        });
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+    uint64_t total = 0;
+    for (uint64_t v : chunk_hits) total += v;
+    if (hits_out) *hits_out = total;
+    return 0;
+}
+
 }  // extern "C"

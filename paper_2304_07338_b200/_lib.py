@@ -67,6 +67,11 @@ class TraceDesc(C.Structure):
                 ("seed", C.c_uint64)]
 
 _P = C.c_void_p
+class PathDesc(C.Structure):
+    _fields_ = [("max_bounces", C.c_int), ("rr_start_bounce", C.c_int), ("rr_min_survival", C.c_double),
+                ("rr_max_survival", C.c_double)]
+
+
 _SIG = {
     "pf_last_error": (C.c_char_p, []),
     "pf_version": (C.c_char_p, []),
@@ -86,6 +91,10 @@ _SIG = {
     "pf_camera_make": (C.c_int, [_P, _P, _P, C.c_double, C.c_int, C.c_int, C.POINTER(Camera)]),
     "pf_render_neural": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), _P,
                                    C.POINTER(RenderStats)]),
+    "pf_render_path_traced": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), C.POINTER(PathDesc),
+                                        _P, C.POINTER(RenderStats)]),
+    "pf_render_photon_map": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), C.c_int, C.c_float,
+                                       _P, C.POINTER(RenderStats)]),
     "pf_tiles_count": (C.c_int, [C.POINTER(Camera), C.POINTER(RenderDesc), C.c_int,
                                  C.POINTER(C.c_int)]),
     "pf_tiles_pack": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), _P, _P]),

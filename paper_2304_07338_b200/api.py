@@ -106,6 +106,20 @@ class RenderConfig:
 
 
 @dataclass
+class PathTraceConfig:
+    """render_path_traced's path controls (roulette as in
+    trace_photons, photon.hpp:29-37)."""
+    max_bounces: int = 16
+    rr_start_bounce: int = 3
+    rr_min_survival: float = 0.05
+    rr_max_survival: float = 0.95
+
+    def c(self) -> _lib.PathDesc:
+        return _lib.PathDesc(self.max_bounces, self.rr_start_bounce, float(self.rr_min_survival),
+                             float(self.rr_max_survival))
+
+
+@dataclass
 class TraceConfig:
     """pf::TraceConfig (proj/include/pf/photon.hpp:29-37)."""
     n_total: int = 100000
@@ -258,6 +272,33 @@ class Context:
         st = _lib.RenderStats()
         check(lib().pf_render_neural(self._h, C.byref(cam), C.byref(cfg.c()), po,
                                      C.byref(st) if stats else None))
+        if stats:
+            return out, {k: getattr(st, k) for k, _ in _lib.RenderStats._fields_}
+        return out
+
+    def render_path_traced(self, cam: _lib.Camera | CameraSpec, cfg: RenderConfig,
+                           path: PathTraceConfig | None = None, out=None, stats: bool = False):
+        """render_path_traced: NEE at every vertex, HG continuation."""
+        if isinstance(cam, CameraSpec):
+            cam = self.camera(cam)
+        path = path or PathTraceConfig()
+        po, out = _out(out, (cam.height, cam.width, 3), np.float32)
+        st = _lib.RenderStats()
+        check(lib().pf_render_path_traced(self._h, C.byref(cam), C.byref(cfg.c()), C.byref(path.c()), po,
+                                          C.byref(st) if stats else None))
+        if stats:
+            return out, {k: getattr(st, k) for k, _ in _lib.RenderStats._fields_}
+        return out
+
+    def render_photon_map(self, cam: _lib.Camera | CameraSpec, cfg: RenderConfig, K: int = 64,
+                          r_max: float = float("inf"), out=None, stats: bool = False):
+        """render_photon_map: L_i from Eq. 6 over the resident map."""
+        if isinstance(cam, CameraSpec):
+            cam = self.camera(cam)
+        po, out = _out(out, (cam.height, cam.width, 3), np.float32)
+        st = _lib.RenderStats()
+        check(lib().pf_render_photon_map(self._h, C.byref(cam), C.byref(cfg.c()), int(K), float(r_max), po,
+                                         C.byref(st) if stats else None))
         if stats:
             return out, {k: getattr(st, k) for k, _ in _lib.RenderStats._fields_}
         return out

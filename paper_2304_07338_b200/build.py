@@ -25,6 +25,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 SOURCES = {
     "pf_trace_parity.cu": ["--fmad=false"],
     "pf_trace_fast.cu": [],
+    "pf_pathtrace_parity.cu": ["--fmad=false"],
+    "pf_pathtrace_fast.cu": [],
     "pf_field.cu": [],
     "pf_compose.cu": [],
     "pf_knn.cu": ["--fmad=false"],

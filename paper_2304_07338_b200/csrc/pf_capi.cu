@@ -31,6 +31,10 @@ cudaError_t launch_delta_track_batch_parity(const DevScene &, const BatchParams 
 cudaError_t launch_delta_track_batch_fast(const DevScene &, const BatchParams &, cudaStream_t);
 int trace_grid_size_parity(int device);
 int trace_grid_size_fast(int device);
+cudaError_t launch_render_pt_parity(const DevScene &, const TraceParams &, int, cudaStream_t);
+cudaError_t launch_render_pt_fast(const DevScene &, const TraceParams &, int, cudaStream_t);
+int pt_grid_size_parity(int device);
+int pt_grid_size_fast(int device);
 }  // namespace pfk
 
 using namespace pfk;
@@ -158,7 +162,7 @@ struct pf_ctx {
     size_t f_smem = 0;
     int sms = 0;
     // render scratch
-    DevBuf slots, hits, counters, frame_stage, stage[8];
+    DevBuf slots, hits, hit_dir, counters, frame_stage, stage[8];
     // knn
     bool has_knn = false;
     KnnParams knn{};
@@ -678,18 +682,39 @@ static ComposeParams compose_params(const pf_camera *cam, const pf_render_desc *
     return C;
 }
 
-int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, float *out_rgb,
-                     pf_render_stats *stats) {
-    if (!c || !cam || !d || !out_rgb) return set_err(PF_ERR_INVALID, "pf_render_neural: null argument");
+// L_i source of the three first-interaction renderers
+enum LiSource { kLiNeural = 0, kLiPathTraced = 1, kLiPhotonMap = 2 };
+
+static int render_common(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, LiSource src,
+                         const pf_path_desc *pt, int K, float r_max, float *out_rgb, pf_render_stats *stats) {
+    const char *name = src == kLiNeural ? "render_neural" : (src == kLiPathTraced ? "render_path_traced"
+                                                                                  : "render_photon_map");
+    if (!c || !cam || !d || !out_rgb) return set_err(PF_ERR_INVALID, "%s: null argument", name);
     if (int e = validate_tiles(cam, d)) return e;
-    if (d->spp <= 0) return set_err(PF_ERR_INVALID, "render_neural: spp must be >= 1");
-    if (!c->vol_tex || !c->has_medium) return set_err(PF_ERR_INVALID, "render_neural: volume/medium not set");
-    if (c->lights.empty()) return set_err(PF_ERR_INVALID, "render_neural: at least one light required");
+    if (d->spp <= 0) return set_err(PF_ERR_INVALID, "%s: spp must be >= 1", name);
+    if (!c->vol_tex || !c->has_medium) return set_err(PF_ERR_INVALID, "%s: volume/medium not set", name);
+    if (c->lights.empty()) return set_err(PF_ERR_INVALID, "%s: at least one light required", name);
     if (d->mode != PF_MODE_PARITY && d->mode != PF_MODE_FAST) return set_err(PF_ERR_INVALID, "render: bad mode");
     if (d->mode == PF_MODE_PARITY && d->nee_trials <= 0)
         return set_err(PF_ERR_INVALID, "transmittance: n_trials must be positive");
-    if (d->use_field && !c->has_field) return set_err(PF_ERR_INVALID, "render_neural: no field loaded");
-    if (!std::isfinite(d->g)) return set_err(PF_ERR_INVALID, "render_neural: non-finite g");
+    if (src == kLiNeural && d->use_field && !c->has_field)
+        return set_err(PF_ERR_INVALID, "render_neural: no field loaded");
+    if (!std::isfinite(d->g)) return set_err(PF_ERR_INVALID, "%s: non-finite g", name);
+    int render_g = -1;
+    if (src == kLiPathTraced) {
+        if (!pt) return set_err(PF_ERR_INVALID, "render_path_traced: null path description");
+        if (pt->max_bounces < 1) return set_err(PF_ERR_INVALID, "render_path_traced: max_bounces must be >= 1");
+        if (!(pt->rr_min_survival > 0.0 && pt->rr_min_survival <= pt->rr_max_survival && pt->rr_max_survival <= 1.0))
+            return set_err(PF_ERR_INVALID, "render_path_traced: need 0 < rr_min_survival <= rr_max_survival <= 1");
+    }
+    if (src == kLiPhotonMap) {
+        if (!c->has_knn) return set_err(PF_ERR_INVALID, "render_photon_map: call pf_knn_build first");
+        if (K < 1 || K > 1024) return set_err(PF_ERR_INVALID, "KnnQuery: K must be in [1, 1024]");
+        if (!(r_max > 0.0f)) return set_err(PF_ERR_INVALID, "KnnQuery: r_max must be > 0");
+        for (int i = 0; i < c->knn.n_phases; ++i)
+            if (c->knn.phase[i] == d->g) render_g = i;
+        if (render_g < 0) return set_err(PF_ERR_INVALID, "render_photon_map: g is not in the map's phase set");
+    }
     PF_CUDA(cudaSetDevice(c->device));
     const bool parity = d->mode == PF_MODE_PARITY;
     ComposeParams C = compose_params(cam, d);
@@ -698,7 +723,9 @@ int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, f
     if (n_work >= (1ull << 32)) return set_err(PF_ERR_INVALID, "render: > 2^32 samples per shard");
     const size_t slot_bytes = n_work * 3 * (parity ? 8 : 4);
     PF_CUDA(c->slots.ensure(slot_bytes));
-    if (d->use_field) PF_CUDA(c->hits.ensure(n_work * sizeof(HitRec)));
+    const bool want_hits = (src == kLiNeural && d->use_field) || src == kLiPhotonMap;
+    if (want_hits) PF_CUDA(c->hits.ensure(n_work * sizeof(HitRec)));
+    if (src == kLiPhotonMap) PF_CUDA(c->hit_dir.ensure(n_work * 24));
     void *frame;
     bool host_out;
     PF_CUDA(c->out_ptr(7, out_rgb, (size_t)cam->width * cam->height * 12, &frame, &host_out));
@@ -728,22 +755,51 @@ int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, f
     P.g = d->g;
     P.w_d = d->w_d;
     P.nee_trials = d->nee_trials > 0 ? d->nee_trials : 1;
-    P.use_field = d->use_field;
+    P.use_field = want_hits ? 1 : 0;
     P.slots = c->slots.p;
     P.hits = (HitRec *)c->hits.p;
+    P.hit_dir = src == kLiPhotonMap ? (double *)c->hit_dir.p : nullptr;
     P.counters = (unsigned long long *)c->counters.p;
+    P.w_i = d->w_i;
+    if (src == kLiPathTraced) {
+        P.init_pt = stream_initstate(d->seed, PF_STREAM_PATHTRACE);
+        P.max_bounces = pt->max_bounces;
+        P.rr_start = pt->rr_start_bounce;
+        P.rr_min = pt->rr_min_survival;
+        P.rr_max = pt->rr_max_survival;
+    }
     const DevScene S = c->scene();
 
     uint32_t n_launch = 0;
     if (c->timing) cudaEventRecord(c->ev[0], c->stream);
-    if (n_work) {
+    if (n_work && src == kLiPathTraced) {
+        ++n_launch;
+        const int grid = parity ? pt_grid_size_parity(c->device) : pt_grid_size_fast(c->device);
+        PF_CUDA(parity ? launch_render_pt_parity(S, P, grid, c->stream) : launch_render_pt_fast(S, P, grid, c->stream));
+    } else if (n_work) {
         ++n_launch;
         const int grid = parity ? trace_grid_size_parity(c->device) : trace_grid_size_fast(c->device);
         PF_CUDA(parity ? launch_render_trace_parity(S, P, grid, c->stream)
                        : launch_render_trace_fast(S, P, grid, c->stream));
     }
     if (c->timing) cudaEventRecord(c->ev[1], c->stream);
-    if (d->use_field && n_work) {
+    if (src == kLiPhotonMap && n_work) {
+        KnnParams Q = c->knn;
+        Q.nq = n_work;  // upper bound; the kernel reads the device-side hit count
+        Q.K = K;
+        Q.r2 = r_max * r_max;
+        Q.order = nullptr;
+        Q.hits = P.hits;
+        Q.hit_dir = P.hit_dir;
+        Q.n_hits = P.counters + 1;
+        Q.slots = c->slots.p;
+        Q.slot_f64 = parity ? 1 : 0;
+        Q.render_g = render_g;
+        Q.w_i = d->w_i;
+        PF_CUDA(knn_query_render(Q, c->sms, c->stream));
+        ++n_launch;
+    }
+    if (src == kLiNeural && d->use_field && n_work) {
         FieldParams F = field_params(c);
         F.mode = 0;
         F.hits = P.hits;
@@ -797,6 +853,21 @@ int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, f
     }
     PF_CUDA(cudaGetLastError());
     return PF_OK;
+}
+
+int pf_render_neural(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, float *out_rgb,
+                     pf_render_stats *stats) {
+    return render_common(c, cam, d, kLiNeural, nullptr, 0, 0.0f, out_rgb, stats);
+}
+
+int pf_render_path_traced(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, const pf_path_desc *pt,
+                          float *out_rgb, pf_render_stats *stats) {
+    return render_common(c, cam, d, kLiPathTraced, pt, 0, 0.0f, out_rgb, stats);
+}
+
+int pf_render_photon_map(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, int K, float r_max,
+                         float *out_rgb, pf_render_stats *stats) {
+    return render_common(c, cam, d, kLiPhotonMap, nullptr, K, r_max, out_rgb, stats);
 }
 
 int pf_tiles_pack(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, const float *frame, float *packed) {

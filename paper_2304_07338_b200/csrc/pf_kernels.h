@@ -55,7 +55,12 @@ struct TraceParams {
     int nee_trials, use_field;
     void *slots;                    // 3 x (double | float) per work item
     HitRec *hits;
+    double *hit_dir;                // optional: omega_out per hit record (photon-map L_i source)
     unsigned long long *counters;   // [0] work, [1] hits, [2] primary steps, [3] shadow steps
+    // render_path_traced only: continuation stream + roulette
+    uint64_t init_pt;
+    int max_bounces, rr_start;
+    double rr_min, rr_max, w_i;
 };
 
 struct BatchParams {

@@ -18,6 +18,8 @@
 //
 // Compiled with --fmad=false: d2 = ((dx*dx)+(dy*dy))+(dz*dz) in binary32 and
 // Eq. 6 in binary64 must round exactly like the oracle.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -173,18 +175,32 @@ __device__ __forceinline__ double knn_hg_eval(double g, double c) {
     return (1.0 / (4.0 * 3.14159265358979323846)) * (1.0 - g * g) / (denom * sqrt(denom));
 }
 
-template <int KP>
+template <int KP, bool RENDER>
 __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
     // per-warp staging buffer: accepted candidates are merged 32 at a time
     __shared__ uint64_t s_buf[4][32];
     const unsigned lane = threadIdx.x & 31u;
     uint64_t *buf = s_buf[(threadIdx.x >> 5) & 3];
-    const size_t qs = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (qs >= P.nq) return;
+    constexpr bool render = RENDER;
+    const size_t nq = render ? (size_t)*P.n_hits : P.nq;
+    const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t qs = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; qs < nq; qs += nwarps) {
     const size_t qi = P.order ? (size_t)__ldg(P.order + qs) : qs;  // spatially sorted visit order
     const int K = P.K;
-    const float q[3] = {P.qx[3 * qi], P.qx[3 * qi + 1], P.qx[3 * qi + 2]};
-    const int g = P.qg[qi];
+    float q[3];
+    int g;
+    if constexpr (render) {
+        const HitRec &h = P.hits[qi];
+        q[0] = h.x[0];
+        q[1] = h.x[1];
+        q[2] = h.x[2];
+        g = P.render_g;
+    } else {
+        q[0] = P.qx[3 * qi];
+        q[1] = P.qx[3 * qi + 1];
+        q[2] = P.qx[3 * qi + 2];
+        g = P.qg[qi];
+    }
     WarpTopK<KP> top;
     top.init();
     int count = 0;
@@ -301,14 +317,15 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
         }
     }
     if (P.out_counts && lane == 0) P.out_counts[qi] = count;
-    if (!P.out_targets) return;
+    if (!P.out_targets && !render) continue;
 
     // ---- fused Eq. 6 (binary64, sequential in list order) + Eq. 7
     double L[3] = {0.0, 0.0, 0.0};
     if (count > 0) {
         const double r = sqrt((double)__uint_as_float((uint32_t)(top.at(count - 1) >> 32)));
         if (!(r < 1e-6)) {
-            const double w[3] = {P.qw[3 * qi], P.qw[3 * qi + 1], P.qw[3 * qi + 2]};
+            const double *wp = render ? P.hit_dir + 3 * qi : P.qw + 3 * qi;
+            const double w[3] = {wp[0], wp[1], wp[2]};
             const double gv = P.phase[g];
             double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -337,7 +354,19 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
             for (int ch = 0; ch < 3; ++ch) L[ch] = acc[ch] / vol;
         }
     }
-    if (lane == 0) {
+    if (render && lane == 0) {
+        // compose term w_i * (sigma_s * L_i) into the sample's slot
+        const HitRec &h = P.hits[qi];
+        if (P.slot_f64) {
+            double *sl = reinterpret_cast<double *>(P.slots) + 3 * (size_t)h.slot;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) sl[ch] = sl[ch] + P.w_i * (h.sigma_s * L[ch]);
+        } else {
+            float *sl = reinterpret_cast<float *>(P.slots) + 3 * (size_t)h.slot;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) sl[ch] = sl[ch] + (float)(P.w_i * (h.sigma_s * L[ch]));
+        }
+    } else if (lane == 0) {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             const double v = L[ch];
@@ -348,6 +377,7 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
             P.out_targets[3 * qi + ch] = t;
         }
     }
+    }  // query loop
 }
 
 // make_batch query generation (oracle or_make_queries).
@@ -473,12 +503,26 @@ cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {
     if (P.nq == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((P.nq * 32 + 127) / 128);
     const int kp = (P.K + 31) / 32;
-    if (kp <= 1) k_knn_query<1><<<blocks, 128, 0, st>>>(P);
-    else if (kp <= 2) k_knn_query<2><<<blocks, 128, 0, st>>>(P);
-    else if (kp <= 4) k_knn_query<4><<<blocks, 128, 0, st>>>(P);
-    else if (kp <= 8) k_knn_query<8><<<blocks, 128, 0, st>>>(P);
-    else if (kp <= 16) k_knn_query<16><<<blocks, 128, 0, st>>>(P);
-    else k_knn_query<32><<<blocks, 128, 0, st>>>(P);
+    if (kp <= 1) k_knn_query<1, false><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 2) k_knn_query<2, false><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 4) k_knn_query<4, false><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 8) k_knn_query<8, false><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 16) k_knn_query<16, false><<<blocks, 128, 0, st>>>(P);
+    else k_knn_query<32, false><<<blocks, 128, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st) {
+    if (P.nq == 0) return cudaSuccess;
+    // persistent: enough warps to fill the SMs, grid-striding over the device-side hit count
+    const unsigned blocks = (unsigned)std::min<size_t>((P.nq * 32 + 127) / 128, (size_t)sms * 16);
+    const int kp = (P.K + 31) / 32;
+    if (kp <= 1) k_knn_query<1, true><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 2) k_knn_query<2, true><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 4) k_knn_query<4, true><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 8) k_knn_query<8, true><<<blocks, 128, 0, st>>>(P);
+    else if (kp <= 16) k_knn_query<16, true><<<blocks, 128, 0, st>>>(P);
+    else k_knn_query<32, true><<<blocks, 128, 0, st>>>(P);
     return cudaGetLastError();
 }
 

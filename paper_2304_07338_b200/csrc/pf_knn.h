@@ -49,6 +49,15 @@ struct KnnParams {
     float *out_d2;
     int32_t *out_counts;
     double *out_targets;
+    // render_photon_map: queries are the render tracer's hit
+    // records (count on the device), phase = render_g, omega = hit_dir; the
+    // estimate lands in the sample slots as w_i * sigma_s * L (Eq. 6, no Eq. 7).
+    const HitRec *hits;
+    const double *hit_dir;
+    const unsigned long long *n_hits;
+    void *slots;
+    int slot_f64, render_g;
+    double w_i;
 };
 
 struct KnnBuffers {
@@ -61,6 +70,8 @@ cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins
 cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffers &B,
                      cudaStream_t st);
 cudaError_t knn_query(const KnnParams &P, cudaStream_t st);
+// render mode: P.nq = upper bound on the hit count, grid-stride over *P.n_hits
+cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st);
 cudaError_t knn_order(const float *x3, const uint8_t *g, size_t n, KnnBuffers &B, const uint32_t **order,
                       cudaStream_t st);
 cudaError_t knn_make_queries(uint64_t initstate, uint64_t base, size_t batch, int n_phases,

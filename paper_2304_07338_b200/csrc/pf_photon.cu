@@ -16,6 +16,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "pf_photon.h"
+#include "pf_phase.cuh"
 #include "pf_trace.cuh"
 
 namespace cg = cooperative_groups;
@@ -23,46 +24,6 @@ namespace cg = cooperative_groups;
 namespace pfk {
 
 namespace {
-
-constexpr double kTwoPiD = 6.283185307179586476925286766559;
-
-// sample_uniform_sphere (rng.hpp:78-83).
-__device__ __forceinline__ void uniform_sphere(Pcg &r, double out[3]) {
-    const double z = 1.0 - 2.0 * pcg_double(r);
-    const double phi = kTwoPiD * pcg_double(r);
-    const double rr = sqrt(stdmax(0.0, 1.0 - z * z));
-    out[0] = rr * cos(phi);
-    out[1] = rr * sin(phi);
-    out[2] = z;
-}
-
-// orthonormal_basis (Duff et al.) + from_local_frame (math.hpp:113-126).
-__device__ __forceinline__ void from_local(const double n[3], const double l[3], double out[3]) {
-    const double sign = copysign(1.0, n[2]);
-    const double a = -1.0 / (sign + n[2]);
-    const double c = n[0] * n[1] * a;
-    const double t[3] = {1.0 + sign * n[0] * n[0] * a, sign * c, -sign * n[0]};
-    const double b[3] = {c, sign + n[1] * n[1] * a, -n[1]};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) out[k] = t[k] * l[0] + b[k] * l[1] + n[k] * l[2];
-}
-
-// hg_sample_cos (phase.hpp:26-31).
-__device__ __forceinline__ double hg_cos(double g, double u) {
-    g = g < -0.999 ? -0.999 : (g > 0.999 ? 0.999 : g);
-    if (fabs(g) < 1e-6) return 1.0 - 2.0 * u;
-    const double sq = (1.0 - g * g) / (1.0 - g + 2.0 * g * u);
-    const double c = (1.0 + g * g - sq * sq) / (2.0 * g);
-    return c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
-}
-
-// cos/sin of the azimuth and the cone/lobe frame (phase.hpp:34-40).
-__device__ __forceinline__ void frame_dir(const double axis[3], double ct, double u2, double out[3]) {
-    const double st = sqrt(stdmax(0.0, 1.0 - ct * ct));
-    const double phi = kTwoPiD * u2;
-    const double local[3] = {st * cos(phi), st * sin(phi), ct};
-    from_local(axis, local, out);
-}
 
 // emit_direction (photon.hpp:48-50; oracle or_emit_direction).
 __device__ __forceinline__ void emit_dir(const double P[3], Pcg &r, double out[3]) {

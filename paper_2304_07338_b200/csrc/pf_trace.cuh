@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS)
             rec.slot = w;
             rec.sigma_s = (double)(rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / R(3)));
             P.hits[h] = rec;
+            if (P.hit_dir) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = (double)wo[a];
+            }
         } else {
             warp_fetch_add(&P.counters[1], 1u);
         }

@@ -1,0 +1,193 @@
+"""render_path_traced / render_photon_map on the GPU vs the oracle.
+
+Tolerances (same reasoning as test_gpu_render.py):
+  * PARITY: binary64 tracking with the reference's majorant and RNG
+    consumption; frames equal the oracle's except where CUDA's log() rounds
+    a last bit differently from glibc.  Path-traced frames: <= 1% of pixels
+    differ by more than 1e-6 relative, frame RMSE <= 1e-3 x mean.  Photon-map
+    frames (exact KNN + binary64 Eq. 6 in list order): <= 1e-3 of pixels.
+  * max_bounces = 1 / w_i = 0 reproduce render_neural without a field (same
+    program up to the first NEE): byte-for-byte in PARITY (--fmad=false);
+    in FAST nvcc may contract the binary32 NEE arithmetic differently in the
+    two kernels, so pixels agree to 1e-6 relative (last-ulp), same decisions.
+  * FAST (binary32 DDA + ratio tracking): statistical -- frame means within
+    3% of PARITY at high spp, per-pixel RMSE <= 1.3x the parity noise floor.
+"""
+import numpy as np
+import pytest
+
+from paper_2304_07338_b200 import PathTraceConfig, RenderConfig
+from paper_2304_07338_b200.scene import CameraSpec, default_lights, synth_photons, synth_volume, tf_scene_b
+
+pytestmark = pytest.mark.gpu
+
+PHASES = [-0.75, 0.0, 0.75]
+
+
+@pytest.fixture(scope="module")
+def scene(ctx, oracle):
+    vol = synth_volume("sphere_sinusoid", 48)
+    tf = tf_scene_b()
+    ctx.upload_volume(vol)
+    ctx.set_medium(tf, 100.0)
+    ctx.set_lights(default_lights())
+    ph = synth_photons(20000, 3, seed=5)
+    ph["power"] *= 1e-3
+    ctx.knn_build(ph, PHASES)
+    return ctx, oracle.OracleScene(vol, tf, 100.0), ph
+
+
+def _rel_mismatch(a, b, rtol=1e-6):
+    a = a.astype(np.float64)
+    b = b.astype(np.float64)
+    bad = np.abs(a - b) > rtol * np.maximum(np.abs(b), 1e-30)
+    return np.count_nonzero(np.any(bad, axis=2))
+
+
+@pytest.mark.parametrize("w_d", [0.0, 1.0])
+def test_path_traced_parity_matches_oracle(scene, oracle, w_d):
+    ctx, osc, _ = scene
+    cam = CameraSpec(64, 48)
+    rc = RenderConfig(spp=4, g=0.3, seed=21, w_d=w_d, mode="parity", background=(0.05, 0.1, 0.2))
+    img, st = ctx.render_path_traced(cam, rc, PathTraceConfig(), stats=True)
+    ref, ost = oracle.render_path_traced(osc, default_lights(), cam, rc, PathTraceConfig())
+    n_bad = _rel_mismatch(img, ref)
+    rmse = np.sqrt(np.mean((img.astype(np.float64) - ref) ** 2))
+    print("pt parity: pixels >1e-6 rel", n_bad, "rmse", rmse, "mean", ref.mean(), "hits", st["hits"], ost["hits"])
+    assert abs(st["hits"] - ost["hits"]) <= 2
+    assert ref.mean() > 0
+    assert n_bad <= 0.01 * 64 * 48
+    assert rmse <= 1e-3 * ref.mean()
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_path_traced_one_bounce_is_render_neural(scene, mode):
+    ctx, _, _ = scene
+    cam = CameraSpec(80, 60)
+    rc = RenderConfig(spp=2, g=-0.3, seed=3, mode=mode, use_field=False, background=(0.3, 0.2, 0.1))
+    a = ctx.render_path_traced(cam, rc, PathTraceConfig(max_bounces=1))
+    b = ctx.render_neural(cam, rc)
+    if mode == "parity":
+        assert np.array_equal(a, b)
+    else:
+        assert _rel_mismatch(a, b, 1e-6) == 0
+
+
+def test_path_traced_fast_statistically_equal(scene):
+    ctx, _, _ = scene
+    cam = CameraSpec(48, 48)
+    pt = PathTraceConfig()
+
+    def r(mode, seed):
+        return ctx.render_path_traced(cam, RenderConfig(spp=128, g=0.5, seed=seed, w_d=0.0, mode=mode), pt
+                                      ).astype(np.float64)
+    par, par2, fast = r("parity", 1), r("parity", 2), r("fast", 3)
+    noise = np.sqrt(np.mean((par2 - par) ** 2))
+    err = np.sqrt(np.mean((fast - par) ** 2))
+    print("pt fast vs parity rmse", err, "noise", noise, "means", fast.mean(), par.mean(), par2.mean())
+    assert abs(fast.mean() - par.mean()) / par.mean() < 0.03
+    assert err < 1.3 * noise
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_path_traced_shard_invariance(scene, mode):
+    ctx, _, _ = scene
+    cam = CameraSpec(70, 45)
+    import torch
+    full = ctx.render_path_traced(cam, RenderConfig(spp=2, g=0.2, seed=9, mode=mode, tile=(16, 8)))
+    parts = torch.zeros((45, 70, 3), dtype=torch.float32, device="cuda")
+    for s in range(3):
+        ctx.render_path_traced(cam, RenderConfig(spp=2, g=0.2, seed=9, mode=mode, tile=(16, 8), shard_index=s,
+                                                 shard_count=3), out=parts)
+    ctx.synchronize()
+    assert np.array_equal(parts.cpu().numpy().view(np.uint32), full.view(np.uint32))
+
+
+def test_path_traced_argument_errors(scene):
+    ctx, _, _ = scene
+    cam = CameraSpec(8, 8)
+    with pytest.raises(ValueError, match="max_bounces"):
+        ctx.render_path_traced(cam, RenderConfig(), PathTraceConfig(max_bounces=0))
+    with pytest.raises(ValueError, match="rr_min"):
+        ctx.render_path_traced(cam, RenderConfig(), PathTraceConfig(rr_min_survival=0.0))
+    with pytest.raises(ValueError, match="spp"):
+        ctx.render_path_traced(cam, RenderConfig(spp=0))
+
+
+@pytest.mark.parametrize("K,r_max", [(32, float("inf")), (64, 0.08)])
+def test_photon_map_parity_matches_oracle(scene, oracle, K, r_max):
+    ctx, osc, ph = scene
+    cam = CameraSpec(64, 48)
+    rc = RenderConfig(spp=2, g=0.75, seed=17, mode="parity")
+    img, st = ctx.render_photon_map(cam, rc, K=K, r_max=r_max, stats=True)
+    tree = oracle.KdTree(ph)
+    ref, ost = oracle.render_photon_map(osc, default_lights(), ph, 2, K, r_max, cam, rc, tree=tree)
+    n_bad = _rel_mismatch(img, ref, 1e-12)
+    print("pm parity: pixels differing", n_bad, "mean", ref.mean(), "hits", st["hits"], ost["hits"])
+    assert abs(st["hits"] - ost["hits"]) <= 2
+    assert n_bad <= max(3, 1e-3 * 64 * 48)
+
+
+def test_photon_map_without_li_is_render_neural(scene):
+    ctx, _, _ = scene
+    cam = CameraSpec(40, 30)
+    for mode in ("parity", "fast"):
+        a = ctx.render_photon_map(cam, RenderConfig(spp=2, g=0.0, seed=4, mode=mode, w_i=0.0), K=16)
+        b = ctx.render_neural(cam, RenderConfig(spp=2, g=0.0, seed=4, mode=mode, use_field=False))
+        c = ctx.render_photon_map(cam, RenderConfig(spp=2, g=0.0, seed=4, mode=mode), K=16)
+        assert np.array_equal(a, b)
+        assert not np.array_equal(c, b)
+
+
+def test_photon_map_fast_statistically_equal(scene):
+    ctx, _, _ = scene
+    cam = CameraSpec(48, 48)
+
+    def r(mode, seed):
+        return ctx.render_photon_map(cam, RenderConfig(spp=64, g=-0.75, seed=seed, w_d=0.0, mode=mode), K=64
+                                     ).astype(np.float64)
+    par, par2, fast = r("parity", 1), r("parity", 2), r("fast", 3)
+    noise = np.sqrt(np.mean((par2 - par) ** 2))
+    err = np.sqrt(np.mean((fast - par) ** 2))
+    print("pm fast vs parity rmse", err, "noise", noise, "means", fast.mean(), par.mean())
+    assert abs(fast.mean() - par.mean()) / par.mean() < 0.03
+    assert err < 1.3 * noise
+
+
+def test_photon_map_argument_errors(scene):
+    ctx, _, _ = scene
+    cam = CameraSpec(8, 8)
+    with pytest.raises(ValueError, match="phase set"):
+        ctx.render_photon_map(cam, RenderConfig(g=0.5), K=8)
+    with pytest.raises(ValueError, match="K must"):
+        ctx.render_photon_map(cam, RenderConfig(g=0.0), K=0)
+    with pytest.raises(ValueError, match="r_max"):
+        ctx.render_photon_map(cam, RenderConfig(g=0.0), K=8, r_max=0.0)
+
+
+def test_zero_alpha_all_renderers_background(ctx):
+    vol = synth_volume("sphere_sinusoid", 16)
+    ctx.upload_volume(vol)
+    ctx.set_medium(np.array([[0.0, 1, 1, 1, 0.0], [1.0, 1, 1, 1, 0.0]]), 100.0)
+    ctx.set_lights(default_lights())
+    ctx.knn_build(synth_photons(500, 3, seed=1), PHASES)
+    cam = CameraSpec(20, 10)
+    bg = np.broadcast_to(np.float32([0.25, 0.5, 0.75]), (10, 20, 3))
+    for mode in ("parity", "fast"):
+        rc = RenderConfig(spp=2, g=0.0, mode=mode, background=(0.25, 0.5, 0.75), use_field=False)
+        assert np.array_equal(ctx.render_path_traced(cam, rc), bg)
+        assert np.array_equal(ctx.render_photon_map(cam, rc, K=8), bg)
+        assert np.array_equal(ctx.render_neural(cam, rc), bg)
+
+
+def test_photon_map_empty_map_is_direct_light(ctx):
+    vol = synth_volume("sphere_sinusoid", 24)
+    ctx.upload_volume(vol)
+    ctx.set_medium(tf_scene_b(), 100.0)
+    ctx.set_lights(default_lights())
+    ctx.knn_build(synth_photons(1, 3, seed=0)[:0], PHASES)
+    cam = CameraSpec(24, 24)
+    for mode in ("parity", "fast"):
+        a = ctx.render_photon_map(cam, RenderConfig(spp=2, g=0.75, seed=4, mode=mode), K=16)
+        b = ctx.render_neural(cam, RenderConfig(spp=2, g=0.75, seed=4, mode=mode, use_field=False))
+        assert np.array_equal(a, b)
