@@ -340,7 +340,7 @@ def main():
     # ---- extras (rank 0): field-query throughput (part c) and KNN gather (config 3)
     extras = {}
     if not args.no_extras:  # every rank runs its own query shard; rank 0 reports the aggregate
-        extras = bench_extras(ctx, fc, params, peaks, rank, world)
+        extras = bench_extras(ctx, fc, params, peaks, rank, world, cam=cam, rc=rc, frame=frame)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -405,7 +405,7 @@ def _sum_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
-def bench_extras(ctx, fc, params, peaks, rank=0, world=1):
+def bench_extras(ctx, fc, params, peaks, rank=0, world=1, cam=None, rc=None, frame=None):
     """Part (c) photon-field queries/s and the config-3 KNN gather, aggregated
     over the ranks (each rank answers its own 2^22 / 2^20 query shard against
     the replicated field / photon map; weak scaling)."""
@@ -459,6 +459,9 @@ def bench_extras(ctx, fc, params, peaks, rank=0, world=1):
                            "tentative_collisions": st["tentative_collisions"], "precision": "f64",
                            "ranks": world, "scaling": "weak"}
     del tr
+    if cam is not None:
+        ctx.knn_build_traced(tc.phase_set)  # the 1M-photon map just traced
+        out["renderers"] = bench_renderers(ctx, cam, rc, frame, world)
     # config 3: KNN radiance estimate (k = 64) over a 4M-photon 3-phase map,
     # 2^20 device-resident queries per batch, CUDA-event timed
     sys.path.insert(0, str(ROOT / "tools"))
@@ -472,6 +475,43 @@ def bench_extras(ctx, fc, params, peaks, rank=0, world=1):
                      "frac": k["algorithmic_GBps"] / hbm, "per_unit": "2560 B (K=64 x 40-B records) per query"}
     out["knn_gather"] = k
     return out
+
+
+def bench_renderers(ctx, cam, rc, frame, world=1):
+    """The SPEC's comparison renderers on the headline frame (this rank's tiles):
+    render_path_traced (16 vertices, NEE + HG continuation + roulette) -- the
+    paper's path tracer of Table 2 -- and render_photon_map
+    (K = 64 over the traced 1M-photon map), next to
+    render_neural.  CUDA events on the render stream, mean of 3 frames."""
+    import torch
+    from paper_2304_07338_b200 import PathTraceConfig
+
+    def timed(fn, n=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / n
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    neural = timed(lambda: ctx.render_neural(cam, rc, out=frame))
+    pt = PathTraceConfig()
+    path = timed(lambda: ctx.render_path_traced(cam, rc, pt, out=frame))
+    pm = timed(lambda: ctx.render_photon_map(cam, rc, K=64, out=frame))
+    return {"ms_neural": neural, "ms_path_traced": path, "ms_photon_map": pm,
+            "speedup_neural_vs_path_traced": path / neural, "speedup_neural_vs_photon_map": pm / neural,
+            "path_traced": {"max_bounces": pt.max_bounces, "rr_start_bounce": pt.rr_start_bounce},
+            "photon_map": {"photons": "1M traced (Alg. 1), 3 phases", "K": 64, "r_max": "inf"},
+            "mode": rc.mode, "note": "same frame, camera, seed and first interactions for all three"}
 
 
 if __name__ == "__main__":
