@@ -271,6 +271,57 @@ int pf_knn_targets(pf_ctx *ctx, size_t nq, const float *x3, const double *w3,
 int pf_make_batch(pf_ctx *ctx, uint64_t seed, uint64_t step, size_t batch, int K, float r_max,
                   double psi, float *x3, double *w3, uint8_t *gidx, double *targets3);
 
+/* ---- photon-field training ------------------- */
+/* AdamState + the rMSE epsilon of train_step. */
+typedef struct {
+    double lr;            /* 9e-4 */
+    double beta1, beta2;  /* 0.9, 0.99 */
+    double eps;           /* 1e-8 */
+    double decay;         /* 0.92 every decay_interval steps ... */
+    double decay_start;   /* ... after this fraction of total_steps (0.7) */
+    int decay_interval;   /* 25 */
+    double eps_rel;       /* relative-MSE epsilon, 0.01 */
+} pf_adam_desc;
+/* Optimizer state over a flat parameter vector (layout as pf_field_load,
+ * which it also performs); adam NULL = the SPEC defaults.  Master parameters
+ * and moments are binary32 on the device. */
+int pf_train_init(pf_ctx *ctx, const pf_field_desc *desc, const float *params, size_t n,
+                  const pf_adam_desc *adam);
+/* train_step(field, batch, targets, adam): x3 in [0,1]^3,
+ * w_sph2 = (theta/pi, (phi+pi)/2pi), g raw, targets3 in L' space.  loss =
+ * mean over batch x channels of (p - t)^2 / (p_detached^2 + eps_rel), returned
+ * pre-update; full backward through MLP + hash-grid interpolation, sparse
+ * (touched-entry) Adam on the tables, dense on the MLP, lr(step, total).
+ * Every reduction has a fixed order: a step is bit-reproducible. */
+int pf_train_step(pf_ctx *ctx, size_t n, const float *x3, const float *w_sph2, const float *g,
+                  const float *targets3, uint64_t step, uint64_t total_steps, double *loss);
+/* Parity entry: loss + dense gradient (n_params floats, may be NULL) + per
+ * table-entry touched flags (pos entries then dir, may be NULL); no update. */
+int pf_train_grad(pf_ctx *ctx, size_t n, const float *x3, const float *w_sph2, const float *g,
+                  const float *targets3, double *loss, float *grad, uint8_t *touched);
+int pf_train_counts(pf_ctx *ctx, size_t *n_params, size_t *n_table_entries);
+/* Master parameters (host or device memory, n = n_params). */
+int pf_train_params(pf_ctx *ctx, float *out, size_t n);
+/* Master parameters -> the inference field used by pf_field_query / renders. */
+int pf_train_commit(pf_ctx *ctx);
+/* train(field, map, cfg): total_steps x {make_batch on the
+ * resident photon map (queries from make_rng(seed, Train, step*batch + i),
+ * KNN radius from the staggered schedule, Eq. 6 + Eq. 7 targets) ->
+ * train_step}; loss_history (total_steps doubles, may be NULL), cumulative
+ * KNN-sampling vs optimizer device time.  Commits the field at the end. */
+typedef struct {
+    uint64_t total_steps;      /* 3000 */
+    size_t batch;              /* 2^16 paper, 2^12 desk */
+    int K;                     /* 1024 paper, 256 desk */
+    int n_segments;            /* KnnSchedule */
+    const double *seg_end;     /* progress fractions, strictly increasing, last = 1 */
+    const double *seg_radius;  /* strictly increasing radii */
+    double psi;                /* Eq. 7 precision */
+    uint64_t seed;
+} pf_train_desc;
+int pf_train(pf_ctx *ctx, const pf_train_desc *desc, double *loss_history, double *ms_knn,
+             double *ms_step);
+
 #ifdef __cplusplus
 }
 #endif

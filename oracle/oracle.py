@@ -83,6 +83,11 @@ class RenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("hits", C.c_uint64)]
 
 
+class AdamCfg(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("decay", C.c_double), ("decay_start", C.c_double), ("decay_interval", C.c_int)]
+
+
 class PtCfg(C.Structure):
     _fields_ = [("max_bounces", C.c_int), ("rr_start_bounce", C.c_int), ("rr_min_survival", C.c_double),
                 ("rr_max_survival", C.c_double)]
@@ -111,6 +116,7 @@ _SIG = {
                                       _P]),
     "or_rng_doubles": (None, [C.c_uint64, C.c_uint64, C.c_size_t, _P, C.c_int, _P]),
     "or_field_param_count": (C.c_size_t, [_P]),
+    "or_hashgrid_param_count": (C.c_size_t, [_P]),
     "or_field_input_dim": (C.c_int, [_P]),
     "or_field_encode": (None, [_P, _P, _P, _P, C.c_double, _P]),
     "or_field_forward": (None, [_P, _P, C.c_size_t, _P, _P, _P, _P]),
@@ -129,6 +135,9 @@ _SIG = {
                               _P, _P, _P, _P]),
     "or_camera_make": (None, [_P, _P, _P, _P, C.c_double, C.c_int, C.c_int]),
     "or_render_neural": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P]),
+    "or_lr_at": (C.c_double, [_P, C.c_uint64, C.c_uint64]),
+    "or_train_grad": (C.c_double, [_P, _P, C.c_size_t, _P, _P, _P, _P, C.c_double, _P, _P, _P, _P]),
+    "or_adam_update": (None, [_P, _P, _P, _P, _P, _P, _P, C.c_uint64, C.c_uint64]),
     "or_render_path_traced": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P]),
     "or_render_photon_map": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P]),
     "or_hg_sample_cos": (C.c_double, [C.c_double, C.c_double]),
@@ -447,6 +456,65 @@ def ref_render_neural(scene: RefScene, lights, fc, params, cam_spec, rc, rect=No
                                _p(out), C.byref(hits)):
         raise ValueError(ref().ref_last_error().decode())
     return out, {"hits": hits.value}
+
+
+# ------------------------------------------------------------ training --
+
+
+def adam_cfg(a=None) -> AdamCfg:
+    """AdamState hyper-parameters; `a` may carry overrides."""
+    d = dict(lr=9e-4, beta1=0.9, beta2=0.99, eps=1e-8, decay=0.92, decay_start=0.7, decay_interval=25)
+    if a is not None:
+        d.update({k: getattr(a, k) for k in d if hasattr(a, k)})
+    return AdamCfg(d["lr"], d["beta1"], d["beta2"], d["eps"], d["decay"], d["decay_start"], int(d["decay_interval"]))
+
+
+def lr_at(step, total, a=None) -> float:
+    return lib().or_lr_at(C.byref(adam_cfg(a)), int(step), int(total))
+
+
+def _mlp_count(fc) -> int:
+    din = fc.pos.levels * fc.pos.features + fc.dir.levels * fc.dir.features + 1
+    w = fc.width
+    return din * w + w + (fc.hidden_layers - 1) * (w * w + w) + 3 * w + 3
+
+
+def train_grad(fc, params, x3, w2, g, targets3, eps_rel=0.01, want_grad=True, den=None, want_pred=False):
+    """rMSE loss and its dense binary64 gradient (or_train_grad); params binary64.
+    den (n, 3) freezes the detached denominators; want_pred adds the predictions."""
+    cfg = field_cfg(fc)
+    params = np.ascontiguousarray(params, np.float64)
+    x3 = np.ascontiguousarray(x3, np.float64)
+    w2 = np.ascontiguousarray(w2, np.float64)
+    g = np.ascontiguousarray(g, np.float64)
+    t = np.ascontiguousarray(targets3, np.float64)
+    n_ent = _entries(fc)
+    grad = np.zeros(len(params)) if want_grad else None
+    touched = np.zeros(n_ent, np.uint8) if want_grad else None
+    pred = np.zeros((len(g), 3)) if want_pred else None
+    den = np.ascontiguousarray(den, np.float64) if den is not None else None
+    loss = lib().or_train_grad(C.byref(cfg), _p(params), len(g), _p(x3), _p(w2), _p(g), _p(t), float(eps_rel),
+                               _p(grad) if want_grad else None, _p(touched) if want_grad else None,
+                               _p(pred) if want_pred else None, _p(den) if den is not None else None)
+    if want_pred:
+        return loss, grad, touched, pred
+    return loss, grad, touched
+
+
+def _entries(fc) -> int:
+    """Table entries (pos then dir), i.e. table parameters / features."""
+    n = 0
+    for hg in (fc.pos, fc.dir):
+        c = HashCfg(hg.dims, hg.levels, hg.features, hg.base_res, float(hg.growth), hg.log2_table)
+        n += lib().or_hashgrid_param_count(C.byref(c)) // hg.features
+    return n
+
+
+def adam_update(fc, params, grad, touched, m, v, step, total, a=None):
+    """In-place Adam step (or_adam_update) on binary64 params / moments."""
+    cfg = field_cfg(fc)
+    lib().or_adam_update(C.byref(cfg), C.byref(adam_cfg(a)), _p(params), _p(grad), _p(touched), _p(m), _p(v),
+                         int(step), int(total))
 
 
 def _ptcfg(pt) -> PtCfg:

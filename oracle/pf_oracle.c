@@ -504,6 +504,210 @@ void or_dir_to_sph(const double w[3], double out[2]) {
     out[1] = (atan2(w[1], w[0]) + OR_PI) / OR_TWO_PI;
 }
 
+/* ===== training: SPEC.md:403-411 (train_step), 380-383 (AdamState) ========
+ * binary64 throughout (parameters included), so the finite-difference oracle
+ * of SPEC.md:409 applies to it directly; the GPU trainer (binary32 master
+ * parameters) is checked against these gradients. */
+
+/* lr(step) = lr0 * decay^floor(max(0, step - start*T) / interval). */
+double or_lr_at(const or_adam_cfg *a, uint64_t step, uint64_t total) {
+    double s = (double)step - a->decay_start * (double)total;
+    if (s < 0.0) s = 0.0;
+    return a->lr * pow(a->decay, floor(s / (double)a->decay_interval));
+}
+
+/* Corner table offsets (entries, relative to the grid's first entry) and
+ * multilinear weights of one input at every level: the same arithmetic as
+ * or_hashgrid_encode. idx/w hold levels * 2^dims values. */
+static void or_grid_corners(const or_hashgrid_cfg *c, const double *in, uint32_t *idx_out, double *w_out) {
+    static const uint32_t primes[3] = {1u, 2654435761u, 805459861u};
+    const int d = c->dims;
+    const uint32_t Tmask = (1u << c->log2_table) - 1u;
+    const or_level_cache *lc = or_levels(c);
+    size_t off = 0;
+    for (int l = 0; l < c->levels; ++l) {
+        const int N = lc->N[l];
+        int ci[3];
+        double f[3];
+        for (int i = 0; i < d; ++i) {
+            double p = in[i] < 0.0 ? 0.0 : (in[i] > 1.0 ? 1.0 : in[i]);
+            double s = p * N;
+            int cc = (int)floor(s);
+            if (cc > N - 1) cc = N - 1;
+            ci[i] = cc;
+            f[i] = s - (double)cc;
+        }
+        for (int corner = 0; corner < (1 << d); ++corner) {
+            double w = 1.0;
+            uint32_t v[3] = {0, 0, 0};
+            for (int i = 0; i < d; ++i) {
+                int bit = (corner >> i) & 1;
+                w *= bit ? f[i] : (1.0 - f[i]);
+                v[i] = (uint32_t)(ci[i] + bit);
+            }
+            uint32_t idx;
+            if (lc->dense[l]) {
+                uint32_t n1 = (uint32_t)N + 1u;
+                idx = v[0];
+                uint32_t mul = n1;
+                for (int i = 1; i < d; ++i) {
+                    idx += v[i] * mul;
+                    mul *= n1;
+                }
+            } else {
+                uint32_t h = 0;
+                for (int i = 0; i < d; ++i) h ^= v[i] * primes[i];
+                idx = h & Tmask;
+            }
+            idx_out[l * (1 << d) + corner] = (uint32_t)(off + idx);
+            w_out[l * (1 << d) + corner] = w;
+        }
+        off += (size_t)lc->size[l];
+    }
+}
+
+/* Loss (rMSE) of a batch and, if grad != NULL, its gradient
+ * w.r.t. every parameter (dense vector, zero where untouched) and the
+ * per-entry touched flags of the two tables (touched may be NULL). */
+double or_train_grad(const or_field_cfg *c, const double *params, size_t n, const double *x3, const double *w2,
+                     const double *g, const double *targets3, double eps_rel, double *grad,
+                     uint8_t *touched, double *pred_out, const double *den_in) {
+    const int din = or_field_input_dim(c), W = c->width, H = c->hidden_layers;
+    const size_t npos = or_hashgrid_param_count(&c->pos), ndir = or_hashgrid_param_count(&c->dir);
+    const size_t nparams = or_field_param_count(c);
+    const double *mlp = params + npos + ndir;
+    const int Fp = c->pos.features, Fd = c->dir.features;
+    const int cp = 1 << c->pos.dims, cd = 1 << c->dir.dims;
+    if (grad) memset(grad, 0, sizeof(double) * nparams);
+    if (touched) memset(touched, 0, (npos / Fp) + (ndir / Fd));
+    double *a = (double *)malloc(sizeof(double) * (size_t)(din + H * W + 3)); /* a_0 | a_1..a_H | out */
+    double *dz = (double *)malloc(sizeof(double) * (size_t)(W > din ? W : din));
+    double *da = (double *)malloc(sizeof(double) * (size_t)(W > din ? W : din));
+    uint32_t *ip = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(c->pos.levels * cp));
+    uint32_t *id = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(c->dir.levels * cd));
+    double *wp = (double *)malloc(sizeof(double) * (size_t)(c->pos.levels * cp));
+    double *wd = (double *)malloc(sizeof(double) * (size_t)(c->dir.levels * cd));
+    double loss = 0.0;
+    const double inv = 1.0 / (3.0 * (double)n);
+    for (size_t q = 0; q < n; ++q) {
+        /* encode */
+        or_grid_corners(&c->pos, x3 + 3 * q, ip, wp);
+        or_grid_corners(&c->dir, w2 + 2 * q, id, wd);
+        for (int k = 0; k < din; ++k) a[k] = 0.0;
+        for (int l = 0; l < c->pos.levels; ++l)
+            for (int j = 0; j < cp; ++j)
+                for (int f = 0; f < Fp; ++f)
+                    a[l * Fp + f] += wp[l * cp + j] * params[(size_t)ip[l * cp + j] * Fp + f];
+        const int o0 = c->pos.levels * Fp;
+        for (int l = 0; l < c->dir.levels; ++l)
+            for (int j = 0; j < cd; ++j)
+                for (int f = 0; f < Fd; ++f)
+                    a[o0 + l * Fd + f] += wd[l * cd + j] * params[npos + (size_t)id[l * cd + j] * Fd + f];
+        a[din - 1] = (g[q] + 1.0) / 2.0;
+        /* MLP forward, keeping a_l */
+        const double *p = mlp;
+        const double *in = a;
+        int nin = din;
+        double *outp = a + din;
+        for (int L = 0; L <= H; ++L) {
+            const int nout = L < H ? W : 3;
+            for (int o = 0; o < nout; ++o) {
+                double acc = 0.0;
+                for (int k = 0; k < nin; ++k) acc += p[(size_t)o * nin + k] * in[k];
+                acc += p[(size_t)nout * nin + o];
+                outp[o] = (L < H && acc < 0.0) ? 0.0 : acc;
+            }
+            p += (size_t)nout * nin + nout;
+            in = outp;
+            outp += nout;
+            nin = nout;
+        }
+        const double *pred = a + din + (size_t)H * W;
+        for (int ch = 0; ch < 3; ++ch) {
+            const double e = pred[ch] - targets3[3 * q + ch];
+            /* prediction detached; den_in freezes it (finite-difference oracle) */
+            const double den = den_in ? den_in[3 * q + ch] : pred[ch] * pred[ch] + eps_rel;
+            if (pred_out) pred_out[3 * q + ch] = pred[ch];
+            loss += e * e / den;
+            dz[ch] = 2.0 * e / den * inv;
+        }
+        if (!grad) continue;
+        /* MLP backward: layer L maps a_L (nin) -> z_L (nout) */
+        size_t off[16];
+        {
+            size_t o = npos + ndir;
+            int ni = din;
+            for (int L = 0; L <= H; ++L) {
+                const int no = L < H ? W : 3;
+                off[L] = o;
+                o += (size_t)no * ni + no;
+                ni = no;
+            }
+        }
+        for (int L = H; L >= 0; --L) {
+            const int nout = L < H ? W : 3, nin2 = L == 0 ? din : W;
+            const double *aL = L == 0 ? a : a + din + (size_t)(L - 1) * W;
+            double *gW = grad + off[L], *gb = gW + (size_t)nout * nin2;
+            const double *Wl = params + off[L];
+            for (int o = 0; o < nout; ++o) {
+                for (int k = 0; k < nin2; ++k) gW[(size_t)o * nin2 + k] += dz[o] * aL[k];
+                gb[o] += dz[o];
+            }
+            for (int k = 0; k < nin2; ++k) {
+                double s = 0.0;
+                for (int o = 0; o < nout; ++o) s += Wl[(size_t)o * nin2 + k] * dz[o];
+                da[k] = s;
+            }
+            if (L > 0)
+                for (int k = 0; k < nin2; ++k) dz[k] = aL[k] > 0.0 ? da[k] : 0.0; /* relu'(z) = [z > 0] */
+        }
+        /* da = d loss / d feature -> tables */
+        for (int l = 0; l < c->pos.levels; ++l)
+            for (int j = 0; j < cp; ++j) {
+                const size_t e = ip[l * cp + j];
+                for (int f = 0; f < Fp; ++f) grad[e * Fp + f] += wp[l * cp + j] * da[l * Fp + f];
+                if (touched) touched[e] = 1;
+            }
+        for (int l = 0; l < c->dir.levels; ++l)
+            for (int j = 0; j < cd; ++j) {
+                const size_t e = id[l * cd + j];
+                for (int f = 0; f < Fd; ++f) grad[npos + e * Fd + f] += wd[l * cd + j] * da[o0 + l * Fd + f];
+                if (touched) touched[npos / Fp + e] = 1;
+            }
+    }
+    free(a);
+    free(dz);
+    free(da);
+    free(ip);
+    free(id);
+    free(wp);
+    free(wd);
+    return loss * inv;
+}
+
+/* Adam with bias correction on the global step t = step + 1:
+ * MLP parameters always, table parameters only for touched entries (sparse
+ * gradients).  params / m / v updated in place. */
+void or_adam_update(const or_field_cfg *c, const or_adam_cfg *a, double *params, const double *grad,
+                    const uint8_t *touched, double *m, double *v, uint64_t step, uint64_t total) {
+    const size_t npos = or_hashgrid_param_count(&c->pos), ndir = or_hashgrid_param_count(&c->dir);
+    const size_t n = or_field_param_count(c);
+    const double lr = or_lr_at(a, step, total);
+    const double t = (double)(step + 1);
+    const double bc1 = 1.0 - pow(a->beta1, t), bc2 = 1.0 - pow(a->beta2, t);
+    for (size_t i = 0; i < n; ++i) {
+        if (i < npos + ndir) {
+            const size_t e = i < npos ? i / (size_t)c->pos.features
+                                      : npos / (size_t)c->pos.features + (i - npos) / (size_t)c->dir.features;
+            if (!touched[e]) continue;
+        }
+        m[i] = a->beta1 * m[i] + (1.0 - a->beta1) * grad[i];
+        v[i] = a->beta2 * v[i] + (1.0 - a->beta2) * grad[i] * grad[i];
+        const double mh = m[i] / bc1, vh = v[i] / bc2;
+        params[i] -= lr * mh / (sqrt(vh) + a->eps);
+    }
+}
+
 /* ===== estimator: SPEC.md:299-326 ======================================== */
 
 /* Eq. 7 with the L > 1 clamp. */

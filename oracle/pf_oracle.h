@@ -137,6 +137,27 @@ void or_field_infer(const or_field_cfg *c, const float *params, size_t n, const 
 /* Direction -> normalized spherical coordinates. */
 void or_dir_to_sph(const double w[3], double out[2]);
 
+/* ---- training: binary64 parameters ---------------------- */
+typedef struct {
+    double lr;           /* 9e-4 */
+    double beta1, beta2; /* 0.9, 0.99 */
+    double eps;          /* 1e-8 */
+    double decay;        /* 0.92 */
+    double decay_start;  /* 0.7 of total steps */
+    int decay_interval;  /* 25 */
+} or_adam_cfg;
+double or_lr_at(const or_adam_cfg *a, uint64_t step, uint64_t total);
+/* rMSE loss = mean over batch x channels of (p - t)^2 / (p_detached^2 + eps_rel);
+ * grad (may be NULL) = dense d loss / d params; touched[entry] flags table
+ * entries (pos entries first, then dir) that received a contribution.
+ * pred_out (may be NULL) receives the predictions; den_in (may be NULL)
+ * replaces p_detached^2 + eps_rel (frozen denominators for finite differences). */
+double or_train_grad(const or_field_cfg *c, const double *params, size_t n, const double *x3, const double *w2,
+                     const double *g, const double *targets3, double eps_rel, double *grad,
+                     uint8_t *touched, double *pred_out, const double *den_in);
+void or_adam_update(const or_field_cfg *c, const or_adam_cfg *a, double *params, const double *grad,
+                    const uint8_t *touched, double *m, double *v, uint64_t step, uint64_t total);
+
 /* ---- estimator: SPEC.md:282-350 ------------------------------------------- */
 double or_encode_log(double L, double psi);
 double or_decode_log(double Lp, double psi);

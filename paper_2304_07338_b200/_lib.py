@@ -72,6 +72,20 @@ class PathDesc(C.Structure):
                 ("rr_max_survival", C.c_double)]
 
 
+_P_ = C.c_void_p
+
+
+class AdamDesc(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("decay", C.c_double), ("decay_start", C.c_double), ("decay_interval", C.c_int),
+                ("eps_rel", C.c_double)]
+
+
+class TrainDesc(C.Structure):
+    _fields_ = [("total_steps", C.c_uint64), ("batch", C.c_size_t), ("K", C.c_int), ("n_segments", C.c_int),
+                ("seg_end", _P_), ("seg_radius", _P_), ("psi", C.c_double), ("seed", C.c_uint64)]
+
+
 _SIG = {
     "pf_last_error": (C.c_char_p, []),
     "pf_version": (C.c_char_p, []),
@@ -118,6 +132,13 @@ _SIG = {
                                  _P, _P, _P, _P]),
     "pf_make_batch": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_size_t, C.c_int, C.c_float,
                                 C.c_double, _P, _P, _P, _P]),
+    "pf_train_init": (C.c_int, [_P, C.POINTER(FieldDesc), _P, C.c_size_t, C.POINTER(AdamDesc)]),
+    "pf_train_step": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_uint64, C.c_uint64, _P]),
+    "pf_train_grad": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, _P, _P, _P]),
+    "pf_train_counts": (C.c_int, [_P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "pf_train_params": (C.c_int, [_P, _P, C.c_size_t]),
+    "pf_train_commit": (C.c_int, [_P]),
+    "pf_train": (C.c_int, [_P, C.POINTER(TrainDesc), _P, _P, _P]),
 }
 EXPORTS = tuple(_SIG)
 

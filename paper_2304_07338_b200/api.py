@@ -132,6 +132,43 @@ class TraceConfig:
 
 
 @dataclass
+class AdamConfig:
+    """AdamState + the rMSE epsilon of train_step."""
+    lr: float = 9e-4
+    beta1: float = 0.9
+    beta2: float = 0.99
+    eps: float = 1e-8
+    decay: float = 0.92
+    decay_start: float = 0.7
+    decay_interval: int = 25
+    eps_rel: float = 0.01
+
+    def c(self) -> _lib.AdamDesc:
+        return _lib.AdamDesc(self.lr, self.beta1, self.beta2, self.eps, self.decay, self.decay_start,
+                             int(self.decay_interval), self.eps_rel)
+
+
+@dataclass
+class TrainConfig:
+    """TrainConfig + KnnSchedule; default = the paper's 1M-row
+    four-step staggered schedule (PAPER.md table tab:training_target_radii)."""
+    total_steps: int = 3000
+    batch_size: int = 1 << 16
+    K: int = 1024
+    schedule_ends: tuple = (0.36, 0.63, 0.90, 1.0)
+    schedule_radii: tuple = (0.25, 0.50, 2.50, 5.0)
+    psi: float = 5.0
+    seed: int = 0
+
+
+@dataclass
+class TrainResult:
+    loss_history: np.ndarray
+    knn_ms: float       # cumulative make_batch (KNN + Eq. 6/7) device time
+    step_ms: float      # cumulative train_step device time
+
+
+@dataclass
 class TraceResult:
     """pf::TraceResult (photon.hpp:39-46)."""
     photons: Any                 # PHOTON_DTYPE array (host) or uint8 CUDA tensor [n, 40]
@@ -243,6 +280,61 @@ class Context:
         p, keep = _in(params, np.float32)
         check(lib().pf_field_load(self._h, C.byref(cfg.c()), p, int(np.prod(keep.shape))))
         self.field_config = cfg
+
+    # ---- training
+    def train_init(self, cfg: FieldConfig, params, adam: AdamConfig | None = None) -> None:
+        p, keep = _in(params, np.float32)
+        check(lib().pf_train_init(self._h, C.byref(cfg.c()), p, int(np.prod(keep.shape)),
+                                  C.byref(adam.c()) if adam is not None else None))
+        self.field_config = cfg
+
+    def train_counts(self) -> tuple[int, int]:
+        a, b = C.c_size_t(), C.c_size_t()
+        check(lib().pf_train_counts(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def _batch(self, x3, wsph2, g, targets3):
+        px, kx = _in(x3, np.float32)
+        pw, kw = _in(wsph2, np.float32)
+        pg, kg = _in(g, np.float32)
+        pt, kt = _in(targets3, np.float32)
+        return _n(kx), (px, pw, pg, pt), (kx, kw, kg, kt)
+
+    def train_step(self, x3, wsph2, g, targets3, step: int, total_steps: int) -> float:
+        n, ptrs, keep = self._batch(x3, wsph2, g, targets3)
+        loss = C.c_double()
+        check(lib().pf_train_step(self._h, n, *ptrs, int(step), int(total_steps), C.byref(loss)))
+        return loss.value
+
+    def train_grad(self, x3, wsph2, g, targets3):
+        """Parity entry: (loss, dense binary32 gradient, touched flags per table entry)."""
+        n, ptrs, keep = self._batch(x3, wsph2, g, targets3)
+        n_params, n_entries = self.train_counts()
+        grad = np.zeros(n_params, np.float32)
+        touched = np.zeros(n_entries, np.uint8)
+        loss = C.c_double()
+        check(lib().pf_train_grad(self._h, n, *ptrs, C.byref(loss), grad.ctypes.data, touched.ctypes.data))
+        return loss.value, grad, touched
+
+    def train_params(self) -> np.ndarray:
+        n_params, _ = self.train_counts()
+        out = np.zeros(n_params, np.float32)
+        check(lib().pf_train_params(self._h, out.ctypes.data, n_params))
+        return out
+
+    def train_commit(self) -> None:
+        check(lib().pf_train_commit(self._h))
+
+    def train(self, cfg: TrainConfig) -> TrainResult:
+        """train(field, map, cfg) on the resident photon map."""
+        ends = np.ascontiguousarray(cfg.schedule_ends, np.float64)
+        radii = np.ascontiguousarray(cfg.schedule_radii, np.float64)
+        d = _lib.TrainDesc(int(cfg.total_steps), int(cfg.batch_size), int(cfg.K), len(ends), ends.ctypes.data,
+                           radii.ctypes.data, float(cfg.psi), int(cfg.seed))
+        hist = np.zeros(int(cfg.total_steps), np.float64)
+        a, b = C.c_double(), C.c_double()
+        check(lib().pf_train(self._h, C.byref(d), hist.ctypes.data, C.byref(a), C.byref(b)))
+        return TrainResult(hist, a.value, b.value)
 
     def field_query(self, x3, wsph2, g, decoded: bool = True, out=None):
         px, kx = _in(x3, np.float32)

@@ -31,6 +31,7 @@ SOURCES = {
     "pf_compose.cu": [],
     "pf_knn.cu": ["--fmad=false"],
     "pf_photon.cu": ["--fmad=false"],
+    "pf_train.cu": [],
     "pf_capi.cu": [],
 }
 

@@ -23,6 +23,7 @@
 #include "pf_kernels.h"
 #include "pf_knn.h"
 #include "pf_photon.h"
+#include "pf_train.h"
 
 namespace pfk {
 cudaError_t launch_render_trace_parity(const DevScene &, const TraceParams &, int, cudaStream_t);
@@ -171,6 +172,9 @@ struct pf_ctx {
     size_t k_n = 0;
     // photon trace (Alg. 1): resident result + scratch
     DevBuf t_rec, t_rec_photon, t_counts, t_offs, t_tmp, t_out, t_ctr;
+    // field training
+    TrainState train;
+    DevBuf tr_x, tr_w2, tr_g, tr_t, tr_w3, tr_gi, tr_t3d;
     size_t t_n = 0;
     unsigned long long trace_steps = 0;
     uint64_t t_total = 0;
@@ -494,10 +498,16 @@ int pf_field_init(const pf_field_desc *d, uint64_t seed, double embed_scale, dou
     return PF_OK;
 }
 
+static int field_load(pf_ctx *c, const FieldDesc &f, const float *params, size_t n);
+
 int pf_field_load(pf_ctx *c, const pf_field_desc *d, const float *params, size_t n) {
     if (!c || !d || !params) return set_err(PF_ERR_INVALID, "pf_field_load: null argument");
     FieldDesc f = to_fdesc(d);
     if (const char *m = field_validate(f)) return set_err(PF_ERR_INVALID, "%s", m);
+    return field_load(c, f, params, n);
+}
+
+static int field_load(pf_ctx *c, const FieldDesc &f, const float *params, size_t n) {
     const size_t need = field_param_count(f);
     if (n != need) return set_err(PF_ERR_INVALID, "pf_field_load: expected %zu params, got %zu", need, n);
     PF_CUDA(cudaSetDevice(c->device));
@@ -1327,6 +1337,186 @@ int pf_make_batch(pf_ctx *c, uint64_t seed, uint64_t step, size_t batch, int K, 
     if (hg) PF_CUDA(cudaMemcpyAsync(gidx, dg, batch, cudaMemcpyDeviceToHost, c->stream));
     if (hx || hw || hg) PF_CUDA(cudaStreamSynchronize(c->stream));
     return PF_OK;
+}
+
+// ------------------------------------------------------------- training --
+static void adam_defaults(pf_adam_desc &a) {
+    a.lr = 9e-4;
+    a.beta1 = 0.9;
+    a.beta2 = 0.99;
+    a.eps = 1e-8;
+    a.decay = 0.92;
+    a.decay_start = 0.7;
+    a.decay_interval = 25;
+    a.eps_rel = 0.01;
+}
+
+int pf_train_init(pf_ctx *c, const pf_field_desc *d, const float *params, size_t n, const pf_adam_desc *adam) {
+    if (!c || !d || !params) return set_err(PF_ERR_INVALID, "pf_train_init: null argument");
+    FieldDesc f = to_fdesc(d);
+    if (const char *m = field_validate(f)) return set_err(PF_ERR_INVALID, "%s", m);
+    if (n != field_param_count(f))
+        return set_err(PF_ERR_INVALID, "pf_train_init: expected %zu params, got %zu", field_param_count(f), n);
+    pf_adam_desc a;
+    adam_defaults(a);
+    if (adam) a = *adam;
+    if (!(a.lr > 0.0) || !(a.beta1 >= 0.0 && a.beta1 < 1.0) || !(a.beta2 >= 0.0 && a.beta2 < 1.0) || !(a.eps > 0.0) ||
+        !(a.decay > 0.0 && a.decay <= 1.0) || !(a.decay_start >= 0.0) || a.decay_interval < 1 || !(a.eps_rel > 0.0))
+        return set_err(PF_ERR_INVALID, "AdamState: invalid hyper-parameters");
+    // the inference field shares the layout: load it too (render/query see the initial field)
+    if (int e = field_load(c, f, params, n)) return e;
+    PF_CUDA(cudaSetDevice(c->device));
+    TrainState &S = c->train;
+    S.lr = a.lr;
+    S.beta1 = a.beta1;
+    S.beta2 = a.beta2;
+    S.eps = a.eps;
+    S.decay = a.decay;
+    S.decay_start = a.decay_start;
+    S.decay_interval = a.decay_interval;
+    S.eps_rel = a.eps_rel;
+    const void *dp;
+    PF_CUDA(c->stage_in(0, params, n * 4, &dp));
+    PF_CUDA(train_init(S, f, c->fhost.levels, (const float *)dp, c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+static int train_common(pf_ctx *c, size_t n, const float *x3, const float *w2, const float *g, const float *t3,
+                        uint64_t step, uint64_t total, bool update, double *loss, float *grad, uint8_t *touched) {
+    if (!c || (n && (!x3 || !w2 || !g || !t3))) return set_err(PF_ERR_INVALID, "train_step: null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "train_step: call pf_train_init first");
+    if (n == 0) return set_err(PF_ERR_INVALID, "train_step: empty batch");
+    if (update && (total == 0 || step >= total)) return set_err(PF_ERR_INVALID, "train_step: need 0 <= step < total");
+    PF_CUDA(cudaSetDevice(c->device));
+    TrainState &S = c->train;
+    const void *dx, *dw, *dg, *dt;
+    PF_CUDA(c->stage_in(0, x3, n * 12, &dx));
+    PF_CUDA(c->stage_in(1, w2, n * 8, &dw));
+    PF_CUDA(c->stage_in(2, g, n * 4, &dg));
+    PF_CUDA(c->stage_in(3, t3, n * 12, &dt));
+    void *dgrad = nullptr, *dtouch = nullptr;
+    bool hgrad = false, htouch = false;
+    if (grad) PF_CUDA(c->out_ptr(4, grad, S.n_params * 4, &dgrad, &hgrad));
+    if (touched) PF_CUDA(c->out_ptr(5, touched, S.n_entries, &dtouch, &htouch));
+    PF_CUDA(S.loss_dev.ensure(8));
+    PF_CUDA(train_step(S, n, (const float *)dx, (const float *)dw, (const float *)dg, (const float *)dt, step, total,
+                       update, (float *)dgrad, (uint8_t *)dtouch, 0, c->sms, c->stream));
+    if (hgrad) PF_CUDA(cudaMemcpyAsync(grad, dgrad, S.n_params * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (htouch) PF_CUDA(cudaMemcpyAsync(touched, dtouch, S.n_entries, cudaMemcpyDeviceToHost, c->stream));
+    if (loss) {
+        PF_CUDA(cudaMemcpyAsync(loss, S.loss_dev.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (loss || hgrad || htouch) PF_CUDA(cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+int pf_train_step(pf_ctx *c, size_t n, const float *x3, const float *w_sph2, const float *g, const float *targets3,
+                  uint64_t step, uint64_t total_steps, double *loss) {
+    return train_common(c, n, x3, w_sph2, g, targets3, step, total_steps, true, loss, nullptr, nullptr);
+}
+
+int pf_train_grad(pf_ctx *c, size_t n, const float *x3, const float *w_sph2, const float *g, const float *targets3,
+                  double *loss, float *grad, uint8_t *touched) {
+    return train_common(c, n, x3, w_sph2, g, targets3, 0, 1, false, loss, grad, touched);
+}
+
+int pf_train_counts(pf_ctx *c, size_t *n_params, size_t *n_entries) {
+    if (!c || !n_params || !n_entries) return set_err(PF_ERR_INVALID, "null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "call pf_train_init first");
+    *n_params = c->train.n_params;
+    *n_entries = c->train.n_entries;
+    return PF_OK;
+}
+
+int pf_train_params(pf_ctx *c, float *out, size_t n) {
+    if (!c || !out) return set_err(PF_ERR_INVALID, "pf_train_params: null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train_params: call pf_train_init first");
+    if (n != c->train.n_params) return set_err(PF_ERR_INVALID, "pf_train_params: expected %zu", c->train.n_params);
+    PF_CUDA(cudaSetDevice(c->device));
+    PF_CUDA(cudaMemcpyAsync(out, c->train.params.p, n * 4, cudaMemcpyDefault, c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+int pf_train_commit(pf_ctx *c) {
+    if (!c) return set_err(PF_ERR_INVALID, "null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train_commit: call pf_train_init first");
+    PF_CUDA(cudaSetDevice(c->device));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
+    return field_load(c, c->train.fd, (const float *)c->train.params.p, c->train.n_params);
+}
+
+int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms_knn, double *ms_step) {
+    if (!c || !d) return set_err(PF_ERR_INVALID, "pf_train: null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train: call pf_train_init first");
+    if (d->total_steps < 1 || d->batch < 1) return set_err(PF_ERR_INVALID, "TrainConfig: total_steps, batch >= 1");
+    if (d->n_segments < 1 || !d->seg_end || !d->seg_radius)
+        return set_err(PF_ERR_INVALID, "KnnSchedule: at least one segment");
+    for (int i = 0; i < d->n_segments; ++i) {
+        if (!(d->seg_end[i] > 0.0 && d->seg_end[i] <= 1.0) || (i && !(d->seg_end[i] > d->seg_end[i - 1])))
+            return set_err(PF_ERR_INVALID, "KnnSchedule: fractions must be strictly increasing in (0, 1]");
+        if (!(d->seg_radius[i] > 0.0) || (i && !(d->seg_radius[i] > d->seg_radius[i - 1])))
+            return set_err(PF_ERR_INVALID, "KnnSchedule: radii must be positive and strictly increasing");
+    }
+    if (d->seg_end[d->n_segments - 1] != 1.0) return set_err(PF_ERR_INVALID, "KnnSchedule: last fraction must be 1");
+    if (d->K < 1 || d->K > 1024) return set_err(PF_ERR_INVALID, "KnnQuery: K must be in [1, 1024]");
+    if (!(d->psi > 0.0)) return set_err(PF_ERR_INVALID, "EncodingConfig: psi must be positive");
+    if (!c->has_knn) return set_err(PF_ERR_INVALID, "pf_train: call pf_knn_build first");
+    PF_CUDA(cudaSetDevice(c->device));
+    TrainState &S = c->train;
+    const size_t B = d->batch;
+    PF_CUDA(c->tr_x.ensure(B * 12));
+    PF_CUDA(c->tr_w3.ensure(B * 24));
+    PF_CUDA(c->tr_gi.ensure(B));
+    PF_CUDA(c->tr_t3d.ensure(B * 24));
+    PF_CUDA(c->tr_w2.ensure(B * 8));
+    PF_CUDA(c->tr_g.ensure(B * 4));
+    PF_CUDA(c->tr_t.ensure(B * 12));
+    PF_CUDA(S.loss_dev.ensure(d->total_steps * 8));
+    cudaEvent_t ev[3];
+    for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
+    double knn_ms = 0.0, step_ms = 0.0;
+    const uint64_t init = stream_initstate(d->seed, PF_STREAM_TRAIN);
+    for (uint64_t step = 0; step < d->total_steps; ++step) {
+        // schedule_radius
+        const double progress = (double)(step + 1) / (double)d->total_steps;
+        double r = d->seg_radius[d->n_segments - 1];
+        for (int i = 0; i < d->n_segments; ++i)
+            if (d->seg_end[i] >= progress) {
+                r = d->seg_radius[i];
+                break;
+            }
+        cudaEventRecord(ev[0], c->stream);
+        // make_batch on the device
+        PF_CUDA(knn_make_queries(init, step * (uint64_t)B, B, c->knn.n_phases, (float *)c->tr_x.p,
+                                 (double *)c->tr_w3.p, (uint8_t *)c->tr_gi.p, c->stream));
+        if (int e = knn_run(c, B, (const float *)c->tr_x.p, (const double *)c->tr_w3.p, (const uint8_t *)c->tr_gi.p,
+                            d->K, (float)r, d->psi, (double *)c->tr_t3d.p, nullptr, nullptr, nullptr))
+            return e;
+        cudaEventRecord(ev[1], c->stream);
+        PF_CUDA(train_prep((const double *)c->tr_w3.p, (const uint8_t *)c->tr_gi.p, (const double *)c->tr_t3d.p,
+                           c->knn.phase, c->knn.n_phases, B, (float *)c->tr_w2.p, (float *)c->tr_g.p,
+                           (float *)c->tr_t.p, c->stream));
+        PF_CUDA(train_step(S, B, (const float *)c->tr_x.p, (const float *)c->tr_w2.p, (const float *)c->tr_g.p,
+                           (const float *)c->tr_t.p, step, d->total_steps, true, nullptr, nullptr, (size_t)step, c->sms,
+                           c->stream));
+        cudaEventRecord(ev[2], c->stream);
+        PF_CUDA(cudaEventSynchronize(ev[2]));
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        knn_ms += a;
+        step_ms += b;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    if (loss_history)
+        PF_CUDA(cudaMemcpyAsync(loss_history, S.loss_dev.p, d->total_steps * 8, cudaMemcpyDefault, c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
+    if (ms_knn) *ms_knn = knn_ms;
+    if (ms_step) *ms_step = step_ms;
+    // the renderer / field queries now use the trained field
+    return field_load(c, S.fd, (const float *)S.params.p, S.n_params);
 }
 
 }  // extern "C"

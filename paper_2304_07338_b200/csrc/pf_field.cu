@@ -24,11 +24,11 @@
 #include <vector>
 
 #include "pf_field.h"
+#include "pf_hashgrid.cuh"
 #include "pf_umma.cuh"
 
 namespace pfk {
 
-constexpr uint32_t kPrime1 = 2654435761u, kPrime2 = 805459861u;
 
 template <int F>
 struct Raw;  // one table entry (F fp16 features)
@@ -86,53 +86,6 @@ __device__ __forceinline__ void store_feats(uint32_t A_s, int r, int k, uint32_t
 
 __device__ __forceinline__ void st_shared_zero16(uint32_t a) {
     asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(0u));
-}
-
-// Cell + fractional weights of one level (exact p*N split: s + e == p*N).
-template <int D>
-__device__ __forceinline__ void level_cell(const FieldLevel &L, const float *pin, uint32_t *c, float *f) {
-    const float resf = (float)L.res;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        const float s = pin[i] * resf;
-        const float e = fmaf(pin[i], resf, -s);
-        const float fl = floorf(s);
-        float fr = (s - fl) + e;
-        int ci = (int)fl;
-        if (fr < 0.f) {
-            ci -= 1;
-            fr += 1.f;
-        }
-        if (ci > (int)L.res - 1) {
-            ci = (int)L.res - 1;
-            fr = (s - (float)ci) + e;
-        }
-        c[i] = (uint32_t)ci;
-        f[i] = fr;
-    }
-}
-
-template <int D>
-__device__ __forceinline__ uint32_t corner_index(const FieldLevel &L, const uint32_t *c, int corner) {
-    uint32_t v[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) v[i] = c[i] + (uint32_t)((corner >> i) & 1);
-    if (L.dense) {
-        uint32_t idx = v[0] + L.n1 * v[1];
-        if (D == 3) idx += L.n1 * L.n1 * v[D - 1];
-        return idx;
-    }
-    uint32_t h = v[0] ^ (v[1] * kPrime1);
-    if (D == 3) h ^= v[D - 1] * kPrime2;
-    return h & L.mask;
-}
-
-template <int D>
-__device__ __forceinline__ float corner_weight(const float *f, int corner) {
-    float w = 1.f;
-#pragma unroll
-    for (int i = 0; i < D; ++i) w *= ((corner >> i) & 1) ? f[i] : (1.f - f[i]);
-    return w;
 }
 
 __device__ __forceinline__ void issue_layer(uint32_t a_s, uint32_t b_s, int K, int N, uint32_t tmem_d) {

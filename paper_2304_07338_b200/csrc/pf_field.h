@@ -1,6 +1,7 @@
 // pf_field.h -- photon-field (hash grid + tcgen05 MLP) internals.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
