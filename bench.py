@@ -459,9 +459,15 @@ def bench_extras(ctx, fc, params, peaks, rank=0, world=1, cam=None, rc=None, fra
                            "tentative_collisions": st["tentative_collisions"], "precision": "f64",
                            "ranks": world, "scaling": "weak"}
     del tr
+    sys.path.insert(0, str(ROOT / "tools"))
     if cam is not None:
         ctx.knn_build_traced(tc.phase_set)  # the 1M-photon map just traced
         out["renderers"] = bench_renderers(ctx, cam, rc, frame, world)
+    # f2: paper-scale field training (2^16 queries / step, K = 1024 targets over
+    # the traced map, paper field): make_batch vs train_step device time
+    import bench_train
+    out["field_training"] = bench_train.run(ctx, steps=10)
+    out["field_training"]["ranks"] = world
     # config 3: KNN radiance estimate (k = 64) over a 4M-photon 3-phase map,
     # 2^20 device-resident queries per batch, CUDA-event timed
     sys.path.insert(0, str(ROOT / "tools"))

@@ -137,6 +137,23 @@ class Device {
         return frame;
     }
 
+    // train(field, map, cfg) and its pieces
+    void train_init(const pf_field_desc &desc, const std::vector<float> &params,
+                    const pf_adam_desc *adam = nullptr) {
+        check(pf_train_init(ctx_, &desc, params.data(), params.size(), adam));
+    }
+    double train_step(size_t n, const float *x3, const float *w_sph2, const float *g, const float *targets3,
+                      uint64_t step, uint64_t total_steps) {
+        double loss = 0.0;
+        check(pf_train_step(ctx_, n, x3, w_sph2, g, targets3, step, total_steps, &loss));
+        return loss;
+    }
+    std::vector<double> train(const pf_train_desc &cfg, double *ms_knn = nullptr, double *ms_step = nullptr) {
+        std::vector<double> hist(cfg.total_steps);
+        check(pf_train(ctx_, &cfg, hist.data(), ms_knn, ms_step));
+        return hist;
+    }
+
     // render_path_traced: NEE + HG continuation + roulette.
     std::vector<float> render_path_traced(const pf_camera &cam, const pf_render_desc &desc,
                                           const pf_path_desc &path, pf_render_stats *stats = nullptr) {
