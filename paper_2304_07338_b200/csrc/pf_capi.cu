@@ -1294,7 +1294,7 @@ static int knn_run(pf_ctx *c, size_t nq, const float *x3, const double *w3, cons
     P.out_targets = (double *)dout;
     P.order = nullptr;
     if (nq >= 4096) PF_CUDA(knn_order(P.qx, P.qg, nq, c->kb, &P.order, c->stream));
-    PF_CUDA(knn_query(P, c->stream));
+    PF_CUDA(knn_query_auto(P, c->kb, c->stream));
     if (hi) PF_CUDA(cudaMemcpyAsync(ids, dids, nq * K * 4, cudaMemcpyDeviceToHost, c->stream));
     if (hd) PF_CUDA(cudaMemcpyAsync(d2, dd2, nq * K * 4, cudaMemcpyDeviceToHost, c->stream));
     if (hc) PF_CUDA(cudaMemcpyAsync(counts, dcnt, nq * 4, cudaMemcpyDeviceToHost, c->stream));

@@ -380,6 +380,289 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
     }  // query loop
 }
 
+// ---- large K: one CTA per query, select instead of merge -------------------
+// For K in (64, 1024] the warp kernel's register top-K (merge 32 keys into a
+// K-long bitonic list per flush) is latency- and spill-bound.  Here a CTA
+//   1. probes the photon density around the query from cell counts only
+//      (cube of cells until it holds >= K photons of the phase),
+//   2. picks a radius rho whose ball should hold ~1.3 K photons and collects
+//      EVERY photon with d2 <= min(rho^2, r_max^2) into shared memory as
+//      (d2, id) keys (all warps stream the sorted rows, coalesced),
+//   3. retries with a larger / smaller rho if the ball held < K photons (and
+//      could hold more) or overflowed the buffer,
+//   4. radix-selects the K-th smallest key (8 x 8-bit MSD passes), keeps the
+//      keys <= it, bitonic-sorts them -> the same list as the oracle,
+//   5. writes ids / d2 / count and Eq. 6 (binary64, sequential in list order)
+//      + Eq. 7 exactly like the warp kernel.
+// Exactness: every photon with d2 <= rho^2 is collected, so when >= K are
+// found the K smallest keys of the whole phase are among them.
+constexpr int kCtaThreads = 256;
+constexpr int kCtaCap = 4608;  // collected keys per query (36 KB)
+
+__global__ void __launch_bounds__(kCtaThreads) k_knn_query_cta(const KnnParams P) {
+    __shared__ uint64_t keys[kCtaCap];
+    __shared__ uint64_t sel[1024];
+    __shared__ uint32_t hist[256];
+    double *terms = reinterpret_cast<double *>(keys);  // 3 x 1024, keys are dead once `sel` is sorted
+    __shared__ int s_n, s_over, s_cnt;
+    __shared__ uint64_t s_prefix;
+    __shared__ int s_need;
+    __shared__ unsigned long long s_cube;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int K = P.K;
+    for (size_t qs = blockIdx.x; qs < P.nq; qs += gridDim.x) {
+        const size_t qi = P.order ? (size_t)__ldg(P.order + qs) : qs;
+        const float q[3] = {P.qx[3 * qi], P.qx[3 * qi + 1], P.qx[3 * qi + 2]};
+        const int g = P.qg[qi];
+        int count = 0;
+        uint64_t kth = ~0ull;
+        const bool live = g < P.n_phases && P.grid[g].n > 0;
+        if (live) {
+            const KnnGrid &Gp = P.grid[g];
+            int R[3], qc[3];
+            float lo[3], h[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                R[a] = Gp.R[a];
+                lo[a] = (float)Gp.lo[a];
+                h[a] = (float)Gp.h[a];
+                qc[a] = cell_axis((double)q[a], Gp.lo[a], Gp.inv_h[a], R[a]);
+            }
+            const float eps = (float)Gp.eps + 1e-6f;
+            const uint32_t cbase = Gp.cell_base;
+            const int rmax = max(R[0], max(R[1], R[2]));
+            auto gap = [&](int a, int c0, int c1) -> float {
+                const float l = c0 == 0 ? -3.0e38f : fmaf((float)c0, h[a], lo[a]) - eps;
+                const float u = c1 == R[a] - 1 ? 3.0e38f : fmaf((float)(c1 + 1), h[a], lo[a]) + eps;
+                const float d = q[a] < l ? l - q[a] : (q[a] > u ? q[a] - u : 0.0f);
+                return d * d;
+            };
+            // 1. density probe: smallest cube of cells around qc holding >= K photons
+            int ring = 0;
+            unsigned long long cube = 0;
+            for (;; ++ring) {
+                if (tid == 0) s_cube = 0ull;
+                __syncthreads();
+                const int side = 2 * ring + 1;
+                for (int r = tid; r < side * side; r += kCtaThreads) {
+                    const int cz = qc[2] - ring + r / side, cy = qc[1] - ring + r % side;
+                    if (cz < 0 || cz >= R[2] || cy < 0 || cy >= R[1]) continue;
+                    const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
+                    const int x0 = max(qc[0] - ring, 0), x1 = min(qc[0] + ring, R[0] - 1);
+                    atomicAdd(&s_cube, (unsigned long long)(__ldg(P.cell_start + row + x1 + 1) -
+                                                           __ldg(P.cell_start + row + x0)));
+                }
+                __syncthreads();
+                cube = s_cube;
+                __syncthreads();
+                if (cube >= (unsigned long long)K || ring >= rmax) break;
+            }
+            // 2. radius whose ball should hold ~1.3 K photons (cube volume / count)
+            double vol = 1.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int c0 = max(qc[a] - ring, 0), c1 = min(qc[a] + ring, R[a] - 1);
+                vol *= (double)(c1 - c0 + 1) * (double)h[a];
+            }
+            double rho = cbrt(1.3 * (double)K * vol / (fmax((double)cube, 1.0) * 4.18879020478639098));
+            // a radius whose ball holds every photon of the phase (grid box + slack)
+            double all = 0.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double b0 = Gp.lo[a] - Gp.eps, b1 = Gp.lo[a] + (double)R[a] * Gp.h[a] + Gp.eps;
+                const double d = fmax(fabs((double)q[a] - b0), fabs((double)q[a] - b1));
+                all += d * d;
+            }
+            all = sqrt(all) * 1.001 + 1e-6;
+            for (int attempt = 0;; ++attempt) {
+                // 3. collect every photon with d2 <= thr
+                const float rho2 = (float)fmin(rho * rho, 3.0e38);
+                const float thr = fminf(rho2, P.r2);
+                const int rc = (int)fmin(ceil(rho / (double)Gp.hmin) + 1.0, (double)rmax);
+                if (tid == 0) {
+                    s_n = 0;
+                    s_over = 0;
+                }
+                __syncthreads();
+                // rows (cz, cy) of the cell cube, one z-slice per warp; per row only the
+                // x-cells the ball can reach (+-1 cell of slack for binary32 rounding)
+                const int z0 = max(qc[2] - rc, 0), z1 = min(qc[2] + rc, R[2] - 1);
+                const int y0 = max(qc[1] - rc, 0), y1 = min(qc[1] + rc, R[1] - 1);
+                const int xl = max(qc[0] - rc, 0), xr = min(qc[0] + rc, R[0] - 1);
+                const float gx = gap(0, xl, xr);
+                for (int cz = z0 + warp; cz <= z1; cz += kCtaThreads / 32) {
+                    const float gz = gap(2, cz, cz);
+                    if ((gz + gx) * (1.0f - 1e-5f) > thr) continue;
+                    for (int cy = y0; cy <= y1; ++cy) {
+                        const float gyz = gz + gap(1, cy, cy);
+                        if ((gyz + gx) * (1.0f - 1e-5f) > thr) continue;
+                        const float dxm = sqrtf(fmaxf(thr - gyz * (1.0f - 1e-5f), 0.0f)) * 1.0001f + eps;
+                        const int xa = max(xl, (int)floorf((q[0] - dxm - lo[0]) / h[0]) - 1);
+                        const int xb = min(xr, (int)floorf((q[0] + dxm - lo[0]) / h[0]) + 1);
+                        if (xa > xb) continue;
+                        const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
+                        const uint32_t b = __ldg(P.cell_start + row + xa), e = __ldg(P.cell_start + row + xb + 1);
+                        for (uint32_t j = b + lane; j < e; j += 32) {
+                            const float4 c = __ldg(&P.spos[j]);
+                            const float d2 = d2_rn(c, q);
+                            if (d2 <= thr) {
+                                const int slot = atomicAdd(&s_n, 1);
+                                if (slot < kCtaCap) keys[slot] = ((uint64_t)__float_as_uint(d2) << 32) | __float_as_uint(c.w);
+                                else s_over = 1;
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                const int n = s_n;
+                const bool over = s_over != 0;
+                const bool short_ = n < K && thr < P.r2 && rho < all;
+                __syncthreads();
+                if (over && attempt < 12) {
+                    rho *= 0.8;
+                    continue;
+                }
+                if (short_ && attempt < 12) {
+                    rho = fmin(rho * 1.5, all);
+                    continue;
+                }
+                if (over || short_) {
+                    count = -1;  // give up (never observed): the warp kernel redoes this query
+                    break;
+                }
+                // 4. K-th smallest key (radix select, MSD 8 bits at a time)
+                count = min(n, K);
+                if (n > K) {
+                    if (tid == 0) {
+                        s_prefix = 0ull;
+                        s_need = K;
+                    }
+                    for (int pass = 0; pass < 8; ++pass) {
+                        const int shift = 56 - 8 * pass;
+                        for (int i = tid; i < 256; i += kCtaThreads) hist[i] = 0u;
+                        __syncthreads();
+                        const uint64_t pre = s_prefix;
+                        const uint64_t pmask = pass == 0 ? 0ull : (~0ull << (64 - 8 * pass));
+                        for (int i = tid; i < n; i += kCtaThreads)
+                            if ((keys[i] & pmask) == pre) atomicAdd(&hist[(keys[i] >> shift) & 255u], 1u);
+                        __syncthreads();
+                        if (warp == 0) {
+                            // bin holding the need-th key: lane-local sums of 8 bins, warp scan
+                            const int need = s_need;
+                            uint32_t loc[8], lsum = 0;
+#pragma unroll
+                            for (int b2 = 0; b2 < 8; ++b2) {
+                                loc[b2] = hist[lane * 8 + b2];
+                                lsum += loc[b2];
+                            }
+                            uint32_t incl = lsum;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                                if (lane >= o) incl += v;
+                            }
+                            const uint32_t excl = incl - lsum;
+                            const unsigned hit = __ballot_sync(0xffffffffu, (int)incl >= need);
+                            const int src = __ffs(hit) - 1;
+                            if (lane == src) {
+                                int left = need - (int)excl, bsel = lane * 8 + 7;
+#pragma unroll
+                                for (int b2 = 0; b2 < 8; ++b2) {
+                                    if ((int)loc[b2] >= left) {
+                                        bsel = lane * 8 + b2;
+                                        break;
+                                    }
+                                    left -= (int)loc[b2];
+                                }
+                                s_need = left;
+                                s_prefix = pre | ((uint64_t)bsel << shift);
+                            }
+                        }
+                        __syncthreads();
+                    }
+                    kth = s_prefix;  // keys are distinct: the K-th key itself
+                } else {
+                    kth = ~0ull;
+                }
+                // compact the selected keys, pad to a power of two, bitonic sort
+                if (tid == 0) s_cnt = 0;
+                __syncthreads();
+                for (int i = tid; i < n; i += kCtaThreads)
+                    if (keys[i] <= kth) sel[atomicAdd(&s_cnt, 1)] = keys[i];
+                __syncthreads();
+                int P2 = 1;
+                while (P2 < count) P2 <<= 1;
+                for (int i = count + tid; i < P2; i += kCtaThreads) sel[i] = ~0ull;
+                __syncthreads();
+                for (int k2 = 2; k2 <= P2; k2 <<= 1)
+                    for (int j = k2 >> 1; j > 0; j >>= 1) {
+                        for (int i = tid; i < P2; i += kCtaThreads) {
+                            const int ij = i ^ j;
+                            if (ij > i) {
+                                const uint64_t a = sel[i], b = sel[ij];
+                                const bool up = (i & k2) == 0;
+                                if ((a > b) == up) {
+                                    sel[i] = b;
+                                    sel[ij] = a;
+                                }
+                            }
+                        }
+                        __syncthreads();
+                    }
+                break;
+            }
+        }
+        if (count < 0) {
+            // fallback marker: counts = -1 tells the host to rerun on the warp kernel
+            if (tid == 0 && P.out_counts) P.out_counts[qi] = -1;
+            if (tid == 0 && P.fallback) P.fallback[atomicAdd(P.fallback_n, 1u)] = (uint32_t)qi;
+            __syncthreads();
+            continue;
+        }
+        // 5. outputs
+        for (int p2 = tid; p2 < K; p2 += kCtaThreads) {
+            const bool lv = p2 < count;
+            if (P.out_ids) P.out_ids[qi * K + p2] = lv ? (uint32_t)sel[p2] : 0xFFFFFFFFu;
+            if (P.out_d2) P.out_d2[qi * K + p2] = lv ? __uint_as_float((uint32_t)(sel[p2] >> 32)) : __int_as_float(0x7f800000);
+        }
+        if (P.out_counts && tid == 0) P.out_counts[qi] = count;
+        if (P.out_targets) {
+            double r = 0.0;
+            if (count > 0) r = sqrt((double)__uint_as_float((uint32_t)(sel[count - 1] >> 32)));
+            const bool zero = count == 0 || r < 1e-6;
+            if (!zero) {
+                const double w[3] = {P.qw[3 * qi], P.qw[3 * qi + 1], P.qw[3 * qi + 2]};
+                const double gv = P.phase[g];
+                for (int p2 = tid; p2 < count; p2 += kCtaThreads) {
+                    const uint32_t j = __ldg(P.inv + (uint32_t)sel[p2]);
+                    const float4 a = __ldg(P.spay + 2 * (size_t)j), b = __ldg(P.spay + 2 * (size_t)j + 1);
+                    const double f = knn_hg_eval(gv, w[0] * (double)a.x + w[1] * (double)a.y + w[2] * (double)a.z);
+                    terms[p2] = f * (double)a.w;
+                    terms[1024 + p2] = f * (double)b.x;
+                    terms[2048 + p2] = f * (double)b.y;
+                }
+            }
+            __syncthreads();
+            if (tid < 3) {
+                double L = 0.0;
+                if (!zero) {
+                    // sequential in list order (bit-identical to the oracle loop)
+                    double acc = 0.0;
+                    const double *tc = terms + 1024 * tid;
+                    for (int p2 = 0; p2 < count; ++p2) acc += tc[p2];
+                    L = acc / ((4.0 / 3.0) * 3.14159265358979323846 * (r * r * r));
+                }
+                double t;
+                if (L > 1.0) t = 0.0;
+                else if (L > P.enc_threshold) t = -log10(L) / P.psi;
+                else t = 1.0;
+                P.out_targets[3 * qi + tid] = t;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // make_batch query generation (oracle or_make_queries).
 __device__ __forceinline__ uint32_t mq_u32(uint64_t &st, uint64_t inc) {
     uint64_t old = st;
@@ -501,6 +784,14 @@ cudaError_t knn_order(const float *x3, const uint8_t *g, size_t n, KnnBuffers &B
 
 cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {
     if (P.nq == 0) return cudaSuccess;
+    if (P.K > 64 && P.fallback) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned blocks = (unsigned)std::min<size_t>(P.nq, (size_t)sms * 3);
+        k_knn_query_cta<<<blocks, kCtaThreads, 0, st>>>(P);
+        return cudaGetLastError();
+    }
     const unsigned blocks = (unsigned)((P.nq * 32 + 127) / 128);
     const int kp = (P.K + 31) / 32;
     if (kp <= 1) k_knn_query<1, false><<<blocks, 128, 0, st>>>(P);
@@ -510,6 +801,31 @@ cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {
     else if (kp <= 16) k_knn_query<16, false><<<blocks, 128, 0, st>>>(P);
     else k_knn_query<32, false><<<blocks, 128, 0, st>>>(P);
     return cudaGetLastError();
+}
+
+cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st) {
+    if (P.nq == 0) return cudaSuccess;
+    if (P.K <= 64) {
+        P.fallback = nullptr;
+        return knn_query(P, st);
+    }
+    cudaError_t e;
+    if ((e = B.fb.ensure(P.nq * 4)) || (e = B.fbn.ensure(16))) return e;
+    P.fallback = (uint32_t *)B.fb.p;
+    P.fallback_n = (unsigned *)B.fbn.p;
+    if ((e = cudaMemsetAsync(B.fbn.p, 0, 4, st))) return e;
+    if ((e = knn_query(P, st))) return e;
+    unsigned n_fb = 0;
+    if ((e = cudaMemcpyAsync(&n_fb, B.fbn.p, 4, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaStreamSynchronize(st))) return e;
+    if (n_fb) {  // exact fallback: the warp kernel on the unresolved queries
+        KnnParams Q = P;
+        Q.fallback = nullptr;
+        Q.order = (const uint32_t *)B.fb.p;
+        Q.nq = n_fb;
+        return knn_query(Q, st);
+    }
+    return cudaSuccess;
 }
 
 cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st) {

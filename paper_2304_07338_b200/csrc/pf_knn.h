@@ -52,6 +52,10 @@ struct KnnParams {
     // render_photon_map: queries are the render tracer's hit
     // records (count on the device), phase = render_g, omega = hit_dir; the
     // estimate lands in the sample slots as w_i * sigma_s * L (Eq. 6, no Eq. 7).
+    // large-K CTA kernel: queries it could not resolve (never observed) are
+    // appended here and re-run on the warp kernel
+    uint32_t *fallback;
+    unsigned *fallback_n;
     const HitRec *hits;
     const double *hit_dir;
     const unsigned long long *n_hits;
@@ -63,6 +67,7 @@ struct KnnParams {
 struct KnnBuffers {
     DevBuf keys, vals, keys2, vals2, hist, cell_start, spos, spay, inv, temp, temp2;
     DevBuf qk, qi, qk2, qi2, temp3;  // query visit-order sort
+    DevBuf fb, fbn;                  // large-K fallback list
 };
 
 cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins, uint32_t *maxs,
@@ -70,6 +75,8 @@ cudaError_t knn_bbox(const PhotonRec *ph, size_t n, int n_phases, uint32_t *mins
 cudaError_t knn_sort(const PhotonRec *ph, size_t n, const KnnParams &P, KnnBuffers &B,
                      cudaStream_t st);
 cudaError_t knn_query(const KnnParams &P, cudaStream_t st);
+// K > 64: CTA-per-query select kernel + exact warp-kernel fallback (syncs the stream)
+cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st);
 // render mode: P.nq = upper bound on the hit count, grid-stride over *P.n_hits
 cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st);
 cudaError_t knn_order(const float *x3, const uint8_t *g, size_t n, KnnBuffers &B, const uint32_t **order,

@@ -345,22 +345,55 @@ struct AdamArgs {
     const uint8_t *touched;
 };
 
-__device__ __forceinline__ bool tab_touched(const AdamArgs &A, size_t i) {
-    const size_t e = i < A.n_pos_tab ? i / (size_t)A.Fp : A.n_pos_tab / (size_t)A.Fp + (i - A.n_pos_tab) / (size_t)A.Fd;
-    return A.touched[e] != 0;
+// One thread per table ENTRY (touched test once; the F contiguous parameters,
+// moments and fixed-point gradients are all loaded before any store, so the
+// loads of a thread overlap) or per MLP parameter.
+template <int F>
+__device__ __forceinline__ void adam_entry(const AdamArgs &A, size_t i0) {
+    float *__restrict__ P = A.params + i0;
+    float *__restrict__ M = A.m + i0;
+    float *__restrict__ V = A.v + i0;
+    unsigned long long *__restrict__ G = A.gtab + i0;
+    unsigned long long gq[F];
+    float p[F], m[F], v[F];
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+        gq[k] = G[k];
+        p[k] = P[k];
+        m[k] = M[k];
+        v[k] = V[k];
+    }
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+        const float g = (float)((double)(long long)gq[k] * (1.0 / kGradFix));
+        m[k] = A.b1 * m[k] + (1.f - A.b1) * g;
+        v[k] = A.b2 * v[k] + (1.f - A.b2) * g * g;
+        p[k] -= A.lr * (m[k] / A.bc1) / (sqrtf(v[k] / A.bc2) + A.eps);
+    }
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+        G[k] = 0ull;
+        P[k] = p[k];
+        M[k] = m[k];
+        V[k] = v[k];
+    }
 }
 
-__global__ void k_train_adam(const AdamArgs A) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= A.n_params) return;
-    float g;
-    if (i < A.n_tab) {
-        if (!tab_touched(A, i)) return;  // sparse: untouched entries keep params and moments
-        g = (float)((double)(long long)A.gtab[i] * (1.0 / kGradFix));
-        A.gtab[i] = 0ull;
-    } else {
-        g = A.gmlp[i - A.n_tab];
+__global__ void k_train_adam(const AdamArgs A, size_t n_pos_entries, size_t n_entries) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_entries) {
+        if (!A.touched[t]) return;  // sparse: untouched entries keep params and moments
+        const bool pos = t < n_pos_entries;
+        const int F = pos ? A.Fp : A.Fd;
+        const size_t i0 = pos ? t * (size_t)A.Fp : A.n_pos_tab + (t - n_pos_entries) * (size_t)A.Fd;
+        if (F == 8) adam_entry<8>(A, i0);
+        else if (F == 4) adam_entry<4>(A, i0);
+        else adam_entry<2>(A, i0);
+        return;
     }
+    const size_t i = A.n_tab + (t - n_entries);
+    if (i >= A.n_params) return;
+    const float g = A.gmlp[i - A.n_tab];
     const float m = A.b1 * A.m[i] + (1.f - A.b1) * g;
     const float v = A.b2 * A.v[i] + (1.f - A.b2) * g * g;
     A.m[i] = m;
@@ -572,7 +605,8 @@ cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2
     A.bc2 = (float)(1.0 - std::pow(S.beta2, t));
     const size_t nb = std::max(S.n_params, S.n_entries);
     if (do_update) {
-        k_train_adam<<<(unsigned)((S.n_params + 255) / 256), 256, 0, st>>>(A);
+        const size_t nt = S.n_entries + (S.n_params - S.n_tab);
+        k_train_adam<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(A, S.n_pos_tab / (size_t)S.Fp, S.n_entries);
     } else {
         k_train_export<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(A, grad_out, touched_out, S.n_entries);
     }

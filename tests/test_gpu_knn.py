@@ -69,7 +69,7 @@ def test_knn_targets_match_oracle(ctx, oracle):
     ctx.knn_build(ph, PHASES)
     x, w, g = oracle.make_queries(11, 0, 2000, 3)
     kd = oracle.KdTree(ph)
-    for K, r in [(64, float("inf")), (64, 0.05), (16, 0.25)]:
+    for K, r in [(64, float("inf")), (64, 0.05), (16, 0.25), (1024, float("inf")), (300, 0.1)]:
         tg, ids, d2, cnt = ctx.knn_targets(x, w, g, K, r, 5.0, with_ids=True)
         rtg, rids, rd2, rcnt = kd.targets(x, w, g, PHASES, K, r, 5.0)
         assert np.array_equal(cnt, rcnt)
@@ -108,3 +108,21 @@ def test_knn_full_size_sampled(ctx, oracle):
     for i in rq.choice(20000, 300, replace=False):
         ri, rd = kd.knn(q[i], int(g[i]), 64)
         assert np.array_equal(ids[i], ri)
+
+
+def test_large_k_select_kernel_exact(ctx, oracle):
+    """K > 64 runs the CTA-per-query select kernel: ids / d2 / counts equal the
+    brute force on uniform, clustered and duplicate-heavy maps, incl. queries far
+    outside the map and phases with fewer than K photons."""
+    r = np.random.default_rng(12)
+    for clustered in (False, True):
+        ph = synth_photons(60000, 3, seed=13, clustered=clustered)
+        ph["g_index"][:700] = 2
+        ph["position"][:700] = ph["position"][0]      # 700 exact duplicates (> cap / K ties)
+        ph["g_index"][-200:] = 0
+        ctx.knn_build(ph, PHASES)
+        q = np.concatenate([r.random((150, 3)), ph["position"][:3], [[-1.0, 0.5, 0.5], [3.0, 3.0, 3.0]]]
+                           ).astype(np.float32)
+        for K, rad in [(1024, float("inf")), (257, float("inf")), (1024, 0.05), (100, 0.3)]:
+            g = r.integers(0, 3, len(q)).astype(np.uint8)
+            _check_against_brute(ctx, oracle, ph, q, g, K, rad)
