@@ -19,6 +19,7 @@
 // Compiled with --fmad=false: d2 = ((dx*dx)+(dy*dy))+(dz*dz) in binary32 and
 // Eq. 6 in binary64 must round exactly like the oracle.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
     const unsigned lane = threadIdx.x & 31u;
     uint64_t *buf = s_buf[(threadIdx.x >> 5) & 3];
     constexpr bool render = RENDER;
-    const size_t nq = render ? (size_t)*P.n_hits : P.nq;
+    const size_t nq = (render && !P.order) ? (size_t)*P.n_hits : P.nq;  // order = fallback list
     const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
     for (size_t qs = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; qs < nq; qs += nwarps) {
     const size_t qi = P.order ? (size_t)__ldg(P.order + qs) : qs;  // spatially sorted visit order
@@ -378,6 +379,337 @@ __global__ void __launch_bounds__(128) k_knn_query(const KnnParams P) {
         }
     }
     }  // query loop
+}
+
+// ---- K <= 64: one warp per query, collect-and-sort instead of merge ----------
+// Same idea as the CTA kernel below at warp scale: probe the density from cell
+// counts, collect every photon inside a ball expected to hold ~1.3 K of them
+// into a per-warp shared buffer (ballot-compacted, coalesced row scans), sort
+// the (d2, id) keys with a warp bitonic network and keep the first K.  ~4x
+// fewer instructions per query than merging 32 keys at a time into the
+// register top-K; exact for the same reason (all photons with d2 <= rho^2 are
+// collected).  Queries whose ball cannot be sized within the buffer go to the
+// merge kernel (fallback list).
+constexpr int kSelWarps = 4;
+// PF_KNN_MERGE=1 forces the merge kernel (A/B comparisons)
+static bool knn_sel_disabled() {
+    const char *e = std::getenv("PF_KNN_MERGE");
+    return e && e[0] == '1';
+}
+constexpr int kSelCap = 256;
+
+// Warp bitonic sort of S*32 keys held as r[s] = element s*32 + lane:
+// strides >= 32 exchange registers, smaller strides exchange lanes.
+template <int S>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&r)[S], unsigned lane) {
+#pragma unroll
+    for (int k2 = 2; k2 <= S * 32; k2 <<= 1) {
+#pragma unroll
+        for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+            if (jj >= 32) {
+                const int js = jj >> 5;
+#pragma unroll
+                for (int sI = 0; sI < S; ++sI) {
+                    if (sI & js) continue;
+                    const int i = sI * 32 + (int)lane;
+                    const bool up = (i & k2) == 0;
+                    const uint64_t a = r[sI], b = r[sI | js];
+                    const bool sw = (a > b) == up;
+                    r[sI] = sw ? b : a;
+                    r[sI | js] = sw ? a : b;
+                }
+            } else {
+#pragma unroll
+                for (int sI = 0; sI < S; ++sI) {
+                    const int i = sI * 32 + (int)lane;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, r[sI], jj);
+                    const bool lower = (lane & jj) == 0;
+                    const bool up = (i & k2) == 0;
+                    // lower element keeps min when ascending
+                    const bool take_min = lower == up;
+                    r[sI] = take_min ? (o < r[sI] ? o : r[sI]) : (o > r[sI] ? o : r[sI]);
+                }
+            }
+        }
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void sort_buf(uint64_t *buf, int n, unsigned lane) {
+    uint64_t r[S];
+#pragma unroll
+    for (int sI = 0; sI < S; ++sI) {
+        const int i = sI * 32 + (int)lane;
+        r[sI] = i < n ? buf[i] : ~0ull;
+    }
+    warp_sort_regs<S>(r, lane);
+#pragma unroll
+    for (int sI = 0; sI < S; ++sI) buf[sI * 32 + (int)lane] = r[sI];
+    __syncwarp();
+}
+
+template <int KP, bool RENDER>
+__global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParams P) {
+    __shared__ uint64_t s_keys[kSelWarps][kSelCap];
+    const unsigned lane = threadIdx.x & 31u;
+    const int wi = threadIdx.x >> 5;
+    uint64_t *buf = s_keys[wi];
+    const size_t nq = RENDER ? (size_t)*P.n_hits : P.nq;
+    const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    const int K = P.K;
+    for (size_t qs = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; qs < nq; qs += nwarps) {
+        const size_t qi = P.order ? (size_t)__ldg(P.order + qs) : qs;
+        float q[3];
+        int g;
+        if constexpr (RENDER) {
+            const HitRec &h = P.hits[qi];
+            q[0] = h.x[0];
+            q[1] = h.x[1];
+            q[2] = h.x[2];
+            g = P.render_g;
+        } else {
+            q[0] = P.qx[3 * qi];
+            q[1] = P.qx[3 * qi + 1];
+            q[2] = P.qx[3 * qi + 2];
+            g = P.qg[qi];
+        }
+        int count = 0, n = 0;
+        bool fail = false;
+        if (g < P.n_phases && P.grid[g].n > 0) {
+            const KnnGrid &Gp = P.grid[g];
+            int R[3], qc[3];
+            float lo[3], h[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                R[a] = Gp.R[a];
+                lo[a] = (float)Gp.lo[a];
+                h[a] = (float)Gp.h[a];
+                qc[a] = cell_axis((double)q[a], Gp.lo[a], Gp.inv_h[a], R[a]);
+            }
+            const float eps = (float)Gp.eps + 1e-6f;
+            const uint32_t cbase = Gp.cell_base;
+            const int rmax = max(R[0], max(R[1], R[2]));
+            auto gap = [&](int a, int c0, int c1) -> float {
+                const float l = c0 == 0 ? -3.0e38f : fmaf((float)c0, h[a], lo[a]) - eps;
+                const float u = c1 == R[a] - 1 ? 3.0e38f : fmaf((float)(c1 + 1), h[a], lo[a]) + eps;
+                const float d = q[a] < l ? l - q[a] : (q[a] > u ? q[a] - u : 0.0f);
+                return d * d;
+            };
+            // 1. density probe (cell counts only)
+            int ring = 0;
+            uint32_t cube = 0;
+            for (;; ++ring) {
+                const int side = 2 * ring + 1;
+                uint32_t c = 0;
+                const int x0 = max(qc[0] - ring, 0), x1 = min(qc[0] + ring, R[0] - 1);
+                for (int r = (int)lane; r < side * side; r += 32) {
+                    const int cz = qc[2] - ring + r / side, cy = qc[1] - ring + r % side;
+                    if (cz < 0 || cz >= R[2] || cy < 0 || cy >= R[1]) continue;
+                    const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
+                    c += __ldg(P.cell_start + row + x1 + 1) - __ldg(P.cell_start + row + x0);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                cube = c;
+                if (cube >= (uint32_t)K || ring >= rmax) break;
+            }
+            double vol = 1.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int c0 = max(qc[a] - ring, 0), c1 = min(qc[a] + ring, R[a] - 1);
+                vol *= (double)(c1 - c0 + 1) * (double)h[a];
+            }
+            double rho = cbrt(1.3 * (double)K * vol / (fmax((double)cube, 1.0) * 4.18879020478639098));
+            double all = 0.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double b0 = Gp.lo[a] - Gp.eps, b1 = Gp.lo[a] + (double)R[a] * Gp.h[a] + Gp.eps;
+                const double d = fmax(fabs((double)q[a] - b0), fabs((double)q[a] - b1));
+                all += d * d;
+            }
+            all = sqrt(all) * 1.001 + 1e-6;
+            // 2. collect every photon with d2 <= thr
+            for (int attempt = 0;; ++attempt) {
+                const float rho2 = (float)fmin(rho * rho, 3.0e38);
+                const float thr = fminf(rho2, P.r2);
+                const int rc = (int)fmin(ceil(rho / (double)Gp.hmin) + 1.0, (double)rmax);
+                const int z0 = max(qc[2] - rc, 0), z1 = min(qc[2] + rc, R[2] - 1);
+                const int y0 = max(qc[1] - rc, 0), y1 = min(qc[1] + rc, R[1] - 1);
+                const int xl = max(qc[0] - rc, 0), xr = min(qc[0] + rc, R[0] - 1);
+                const float gx = gap(0, xl, xr);
+                n = 0;
+                bool over = false;
+                // rows of the cube in chunks of 32: each lane sizes one row (ball
+                // pruning, exact x-cell range through the binning function), a warp
+                // scan concatenates the row segments and all 32 lanes stream the
+                // concatenated candidates (independent, coalesced loads)
+                const int ny = y1 - y0 + 1, nrows = (z1 - z0 + 1) * ny;
+                for (int r0 = 0; r0 < nrows && !over; r0 += 32) {
+                    const int r = r0 + (int)lane;
+                    uint32_t b = 0, len = 0;
+                    if (r < nrows) {
+                        const int cz = z0 + r / ny, cy = y0 + r % ny;
+                        const float gyz = gap(2, cz, cz) + gap(1, cy, cy);
+                        if ((gyz + gx) * (1.0f - 1e-5f) <= thr) {
+                            const double dxm = sqrt((double)fmaxf(thr - gyz * (1.0f - 1e-5f), 0.0f)) * 1.00001 + 1e-7;
+                            const int xa = max(xl, cell_axis((double)q[0] - dxm, Gp.lo[0], Gp.inv_h[0], R[0]));
+                            const int xb = min(xr, cell_axis((double)q[0] + dxm, Gp.lo[0], Gp.inv_h[0], R[0]));
+                            if (xa <= xb) {
+                                const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
+                                b = __ldg(P.cell_start + row + xa);
+                                len = __ldg(P.cell_start + row + xb + 1) - b;
+                            }
+                        }
+                    }
+                    uint32_t incl = len;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if ((int)lane >= o) incl += t;
+                    }
+                    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+                        const uint32_t t = t0 + lane;
+                        // segment of candidate t: first lane whose inclusive offset exceeds t
+                        int pos = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const uint32_t v = __shfl_sync(0xffffffffu, incl, pos + step - 1);
+                            if (v <= t) pos += step;
+                        }
+                        const uint32_t seg_b = __shfl_sync(0xffffffffu, b, pos);
+                        const uint32_t seg_excl = __shfl_sync(0xffffffffu, incl - len, pos);
+                        uint64_t key = 0;
+                        bool acc = false;
+                        if (t < total) {
+                            const float4 c = __ldg(&P.spos[seg_b + (t - seg_excl)]);
+                            const float d2 = d2_rn(c, q);
+                            acc = d2 <= thr;
+                            key = ((uint64_t)__float_as_uint(d2) << 32) | __float_as_uint(c.w);
+                        }
+                        const unsigned m = __ballot_sync(0xffffffffu, acc);
+                        const int slot = n + __popc(m & knn_lanemask_lt());
+                        if (acc && slot < kSelCap) buf[slot] = key;
+                        n += __popc(m);
+                    }
+                    if (n > kSelCap) over = true;
+                }
+                const bool short_ = n < K && thr < P.r2 && rho < all;
+                if (over && attempt < 10) {
+                    rho *= 0.75;
+                    continue;
+                }
+                if (short_ && attempt < 10) {
+                    rho = fmin(rho * 1.5, all);
+                    continue;
+                }
+                fail = over || short_;
+                break;
+            }
+            __syncwarp();
+            if (!fail) {
+                // 3. warp bitonic sort of the n keys in registers
+                if (n <= 32) sort_buf<1>(buf, n, lane);
+                else if (n <= 64) sort_buf<2>(buf, n, lane);
+                else if (n <= 128) sort_buf<4>(buf, n, lane);
+                else sort_buf<8>(buf, n, lane);
+                count = min(n, K);
+            }
+        }
+        if (fail) {
+            if (lane == 0) P.fallback[atomicAdd(P.fallback_n, 1u)] = (uint32_t)qi;
+            __syncwarp();
+            continue;
+        }
+        // 4. outputs (list position p = s*32 + lane, like the merge kernel)
+        uint64_t v[KP];
+#pragma unroll
+        for (int sI = 0; sI < KP; ++sI) {
+            const int p2 = sI * 32 + (int)lane;
+            v[sI] = p2 < count ? buf[p2] : ~0ull;
+        }
+        if constexpr (!RENDER) {
+            if (P.out_ids || P.out_d2) {
+#pragma unroll
+                for (int sI = 0; sI < KP; ++sI) {
+                    const int p2 = sI * 32 + (int)lane;
+                    if (p2 < K) {
+                        const bool lv = p2 < count;
+                        if (P.out_ids) P.out_ids[qi * K + p2] = lv ? (uint32_t)v[sI] : 0xFFFFFFFFu;
+                        if (P.out_d2)
+                            P.out_d2[qi * K + p2] = lv ? __uint_as_float((uint32_t)(v[sI] >> 32)) : __int_as_float(0x7f800000);
+                    }
+                }
+            }
+            if (P.out_counts && lane == 0) P.out_counts[qi] = count;
+            if (!P.out_targets) {
+                __syncwarp();
+                continue;
+            }
+        }
+        // fused Eq. 6 (binary64, sequential in list order) + Eq. 7 / compose term
+        double L[3] = {0.0, 0.0, 0.0};
+        if (count > 0) {
+            const double r = sqrt((double)__uint_as_float((uint32_t)(buf[count - 1] >> 32)));
+            if (!(r < 1e-6)) {
+                const double *wp = RENDER ? P.hit_dir + 3 * qi : P.qw + 3 * qi;
+                const double w[3] = {wp[0], wp[1], wp[2]};
+                const double gv = P.phase[g];
+                // per-photon terms -> shared memory (the key buffer is free now), then
+                // lanes 0..2 sum one channel each sequentially in list order
+                double *tb = reinterpret_cast<double *>(buf);  // 3 x 64 doubles <= kSelCap keys
+                __syncwarp();  // every lane has read buf[count - 1] (r) before it is overwritten
+#pragma unroll
+                for (int sI = 0; sI < KP; ++sI) {
+                    const int p2 = sI * 32 + (int)lane;
+                    if (p2 < count) {
+                        const uint32_t j = __ldg(P.inv + (uint32_t)v[sI]);
+                        const float4 a = __ldg(P.spay + 2 * (size_t)j), b = __ldg(P.spay + 2 * (size_t)j + 1);
+                        const double f = knn_hg_eval(gv, w[0] * (double)a.x + w[1] * (double)a.y + w[2] * (double)a.z);
+                        tb[p2] = f * (double)a.w;
+                        tb[64 + p2] = f * (double)b.x;
+                        tb[128 + p2] = f * (double)b.y;
+                    }
+                }
+                __syncwarp();
+                double a2 = 0.0;
+                if (lane < 3)
+                    for (int k = 0; k < count; ++k) a2 += tb[64 * lane + k];
+                __syncwarp();
+                double acc[3];
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) acc[ch] = __shfl_sync(0xffffffffu, a2, ch);
+                const double vol = (4.0 / 3.0) * 3.14159265358979323846 * (r * r * r);
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) L[ch] = acc[ch] / vol;
+            }
+        }
+        if (lane == 0) {
+            if constexpr (RENDER) {
+                const HitRec &hr = P.hits[qi];
+                if (P.slot_f64) {
+                    double *sl = reinterpret_cast<double *>(P.slots) + 3 * (size_t)hr.slot;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) sl[ch] = sl[ch] + P.w_i * (hr.sigma_s * L[ch]);
+                } else {
+                    float *sl = reinterpret_cast<float *>(P.slots) + 3 * (size_t)hr.slot;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) sl[ch] = sl[ch] + (float)(P.w_i * (hr.sigma_s * L[ch]));
+                }
+            } else {
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    const double vv = L[ch];
+                    double t;
+                    if (vv > 1.0) t = 0.0;
+                    else if (vv > P.enc_threshold) t = -log10(vv) / P.psi;
+                    else t = 1.0;
+                    P.out_targets[3 * qi + ch] = t;
+                }
+            }
+        }
+        __syncwarp();
+    }
 }
 
 // ---- large K: one CTA per query, select instead of merge -------------------
@@ -803,13 +1135,41 @@ cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+static int knn_sms() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
 cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st) {
     if (P.nq == 0) return cudaSuccess;
+    cudaError_t e;
+    if (P.K <= 64 && !knn_sel_disabled()) {
+        if ((e = B.fb.ensure(P.nq * 4)) || (e = B.fbn.ensure(16))) return e;
+        P.fallback = (uint32_t *)B.fb.p;
+        P.fallback_n = (unsigned *)B.fbn.p;
+        if ((e = cudaMemsetAsync(B.fbn.p, 0, 4, st))) return e;
+        const unsigned blocks = (unsigned)std::min<size_t>((P.nq + kSelWarps - 1) / kSelWarps, (size_t)knn_sms() * 16);
+        if (P.K <= 32) k_knn_query_sel<1, false><<<blocks, kSelWarps * 32, 0, st>>>(P);
+        else k_knn_query_sel<2, false><<<blocks, kSelWarps * 32, 0, st>>>(P);
+        if ((e = cudaGetLastError())) return e;
+        unsigned n_fb = 0;
+        if ((e = cudaMemcpyAsync(&n_fb, B.fbn.p, 4, cudaMemcpyDeviceToHost, st))) return e;
+        if ((e = cudaStreamSynchronize(st))) return e;
+        if (n_fb) {
+            KnnParams Q = P;
+            Q.fallback = nullptr;
+            Q.order = (const uint32_t *)B.fb.p;
+            Q.nq = n_fb;
+            return knn_query(Q, st);
+        }
+        return cudaSuccess;
+    }
     if (P.K <= 64) {
         P.fallback = nullptr;
         return knn_query(P, st);
     }
-    cudaError_t e;
     if ((e = B.fb.ensure(P.nq * 4)) || (e = B.fbn.ensure(16))) return e;
     P.fallback = (uint32_t *)B.fb.p;
     P.fallback_n = (unsigned *)B.fbn.p;
@@ -828,8 +1188,27 @@ cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st) {
     return cudaSuccess;
 }
 
-cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st) {
-    if (P.nq == 0) return cudaSuccess;
+cudaError_t knn_query_render(const KnnParams &P0, KnnBuffers &B, int sms, cudaStream_t st) {
+    if (P0.nq == 0) return cudaSuccess;
+    KnnParams P = P0;
+    cudaError_t e;
+    if (P.K <= 64 && !knn_sel_disabled()) {
+        if ((e = B.fb.ensure(P.nq * 4)) || (e = B.fbn.ensure(16))) return e;
+        P.fallback = (uint32_t *)B.fb.p;
+        P.fallback_n = (unsigned *)B.fbn.p;
+        if ((e = cudaMemsetAsync(B.fbn.p, 0, 4, st))) return e;
+        const unsigned blocks = (unsigned)std::min<size_t>((P.nq + kSelWarps - 1) / kSelWarps, (size_t)sms * 16);
+        if (P.K <= 32) k_knn_query_sel<1, true><<<blocks, kSelWarps * 32, 0, st>>>(P);
+        else k_knn_query_sel<2, true><<<blocks, kSelWarps * 32, 0, st>>>(P);
+        if ((e = cudaGetLastError())) return e;
+        unsigned n_fb = 0;
+        if ((e = cudaMemcpyAsync(&n_fb, B.fbn.p, 4, cudaMemcpyDeviceToHost, st))) return e;
+        if ((e = cudaStreamSynchronize(st))) return e;
+        if (!n_fb) return cudaSuccess;
+        P.fallback = nullptr;
+        P.order = (const uint32_t *)B.fb.p;  // merge kernel on the unresolved hits
+        P.nq = n_fb;
+    }
     // persistent: enough warps to fill the SMs, grid-striding over the device-side hit count
     const unsigned blocks = (unsigned)std::min<size_t>((P.nq * 32 + 127) / 128, (size_t)sms * 16);
     const int kp = (P.K + 31) / 32;
