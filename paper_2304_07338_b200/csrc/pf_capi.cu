@@ -806,7 +806,7 @@ static int render_common(pf_ctx *c, const pf_camera *cam, const pf_render_desc *
         Q.slot_f64 = parity ? 1 : 0;
         Q.render_g = render_g;
         Q.w_i = d->w_i;
-        PF_CUDA(knn_query_render(Q, c->kb, c->sms, c->stream));
+        PF_CUDA(knn_query_render(Q, c->sms, c->stream));
         ++n_launch;
     }
     if (src == kLiNeural && d->use_field && n_work) {

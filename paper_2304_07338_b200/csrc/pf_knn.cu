@@ -448,31 +448,19 @@ __device__ __forceinline__ void sort_buf(uint64_t *buf, int n, unsigned lane) {
     __syncwarp();
 }
 
-template <int KP, bool RENDER>
+template <int KP>
 __global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParams P) {
     __shared__ uint64_t s_keys[kSelWarps][kSelCap];
     const unsigned lane = threadIdx.x & 31u;
     const int wi = threadIdx.x >> 5;
     uint64_t *buf = s_keys[wi];
-    const size_t nq = RENDER ? (size_t)*P.n_hits : P.nq;
+    const size_t nq = P.nq;
     const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
     const int K = P.K;
     for (size_t qs = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; qs < nq; qs += nwarps) {
         const size_t qi = P.order ? (size_t)__ldg(P.order + qs) : qs;
-        float q[3];
-        int g;
-        if constexpr (RENDER) {
-            const HitRec &h = P.hits[qi];
-            q[0] = h.x[0];
-            q[1] = h.x[1];
-            q[2] = h.x[2];
-            g = P.render_g;
-        } else {
-            q[0] = P.qx[3 * qi];
-            q[1] = P.qx[3 * qi + 1];
-            q[2] = P.qx[3 * qi + 2];
-            g = P.qg[qi];
-        }
+        const float q[3] = {P.qx[3 * qi], P.qx[3 * qi + 1], P.qx[3 * qi + 2]};
+        const int g = P.qg[qi];
         int count = 0, n = 0;
         bool fail = false;
         if (g < P.n_phases && P.grid[g].n > 0) {
@@ -595,12 +583,13 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParam
                     if (n > kSelCap) over = true;
                 }
                 const bool short_ = n < K && thr < P.r2 && rho < all;
+                // resize the ball from what this one held (density-corrected)
                 if (over && attempt < 10) {
-                    rho *= 0.75;
+                    rho *= fmax(0.5, fmin(0.9, cbrt(1.3 * (double)K / (double)n)));
                     continue;
                 }
                 if (short_ && attempt < 10) {
-                    rho = fmin(rho * 1.5, all);
+                    rho = fmin(rho * fmin(3.0, fmax(1.25, cbrt(1.3 * (double)K / fmax((double)n, 1.0)))), all);
                     continue;
                 }
                 fail = over || short_;
@@ -628,31 +617,29 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParam
             const int p2 = sI * 32 + (int)lane;
             v[sI] = p2 < count ? buf[p2] : ~0ull;
         }
-        if constexpr (!RENDER) {
-            if (P.out_ids || P.out_d2) {
+        if (P.out_ids || P.out_d2) {
 #pragma unroll
-                for (int sI = 0; sI < KP; ++sI) {
-                    const int p2 = sI * 32 + (int)lane;
-                    if (p2 < K) {
-                        const bool lv = p2 < count;
-                        if (P.out_ids) P.out_ids[qi * K + p2] = lv ? (uint32_t)v[sI] : 0xFFFFFFFFu;
-                        if (P.out_d2)
-                            P.out_d2[qi * K + p2] = lv ? __uint_as_float((uint32_t)(v[sI] >> 32)) : __int_as_float(0x7f800000);
-                    }
+            for (int sI = 0; sI < KP; ++sI) {
+                const int p2 = sI * 32 + (int)lane;
+                if (p2 < K) {
+                    const bool lv = p2 < count;
+                    if (P.out_ids) P.out_ids[qi * K + p2] = lv ? (uint32_t)v[sI] : 0xFFFFFFFFu;
+                    if (P.out_d2)
+                        P.out_d2[qi * K + p2] = lv ? __uint_as_float((uint32_t)(v[sI] >> 32)) : __int_as_float(0x7f800000);
                 }
             }
-            if (P.out_counts && lane == 0) P.out_counts[qi] = count;
-            if (!P.out_targets) {
-                __syncwarp();
-                continue;
-            }
         }
-        // fused Eq. 6 (binary64, sequential in list order) + Eq. 7 / compose term
+        if (P.out_counts && lane == 0) P.out_counts[qi] = count;
+        if (!P.out_targets) {
+            __syncwarp();
+            continue;
+        }
+        // fused Eq. 6 (binary64, sequential in list order) + Eq. 7
         double L[3] = {0.0, 0.0, 0.0};
         if (count > 0) {
             const double r = sqrt((double)__uint_as_float((uint32_t)(buf[count - 1] >> 32)));
             if (!(r < 1e-6)) {
-                const double *wp = RENDER ? P.hit_dir + 3 * qi : P.qw + 3 * qi;
+                const double *wp = P.qw + 3 * qi;
                 const double w[3] = {wp[0], wp[1], wp[2]};
                 const double gv = P.phase[g];
                 // per-photon terms -> shared memory (the key buffer is free now), then
@@ -685,27 +672,14 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParam
             }
         }
         if (lane == 0) {
-            if constexpr (RENDER) {
-                const HitRec &hr = P.hits[qi];
-                if (P.slot_f64) {
-                    double *sl = reinterpret_cast<double *>(P.slots) + 3 * (size_t)hr.slot;
 #pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) sl[ch] = sl[ch] + P.w_i * (hr.sigma_s * L[ch]);
-                } else {
-                    float *sl = reinterpret_cast<float *>(P.slots) + 3 * (size_t)hr.slot;
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) sl[ch] = sl[ch] + (float)(P.w_i * (hr.sigma_s * L[ch]));
-                }
-            } else {
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    const double vv = L[ch];
-                    double t;
-                    if (vv > 1.0) t = 0.0;
-                    else if (vv > P.enc_threshold) t = -log10(vv) / P.psi;
-                    else t = 1.0;
-                    P.out_targets[3 * qi + ch] = t;
-                }
+            for (int ch = 0; ch < 3; ++ch) {
+                const double vv = L[ch];
+                double t;
+                if (vv > 1.0) t = 0.0;
+                else if (vv > P.enc_threshold) t = -log10(vv) / P.psi;
+                else t = 1.0;
+                P.out_targets[3 * qi + ch] = t;
             }
         }
         __syncwarp();
@@ -1151,8 +1125,8 @@ cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st) {
         P.fallback_n = (unsigned *)B.fbn.p;
         if ((e = cudaMemsetAsync(B.fbn.p, 0, 4, st))) return e;
         const unsigned blocks = (unsigned)std::min<size_t>((P.nq + kSelWarps - 1) / kSelWarps, (size_t)knn_sms() * 16);
-        if (P.K <= 32) k_knn_query_sel<1, false><<<blocks, kSelWarps * 32, 0, st>>>(P);
-        else k_knn_query_sel<2, false><<<blocks, kSelWarps * 32, 0, st>>>(P);
+        if (P.K <= 32) k_knn_query_sel<1><<<blocks, kSelWarps * 32, 0, st>>>(P);
+        else k_knn_query_sel<2><<<blocks, kSelWarps * 32, 0, st>>>(P);
         if ((e = cudaGetLastError())) return e;
         unsigned n_fb = 0;
         if ((e = cudaMemcpyAsync(&n_fb, B.fbn.p, 4, cudaMemcpyDeviceToHost, st))) return e;
@@ -1188,27 +1162,11 @@ cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st) {
     return cudaSuccess;
 }
 
-cudaError_t knn_query_render(const KnnParams &P0, KnnBuffers &B, int sms, cudaStream_t st) {
-    if (P0.nq == 0) return cudaSuccess;
-    KnnParams P = P0;
-    cudaError_t e;
-    if (P.K <= 64 && !knn_sel_disabled()) {
-        if ((e = B.fb.ensure(P.nq * 4)) || (e = B.fbn.ensure(16))) return e;
-        P.fallback = (uint32_t *)B.fb.p;
-        P.fallback_n = (unsigned *)B.fbn.p;
-        if ((e = cudaMemsetAsync(B.fbn.p, 0, 4, st))) return e;
-        const unsigned blocks = (unsigned)std::min<size_t>((P.nq + kSelWarps - 1) / kSelWarps, (size_t)sms * 16);
-        if (P.K <= 32) k_knn_query_sel<1, true><<<blocks, kSelWarps * 32, 0, st>>>(P);
-        else k_knn_query_sel<2, true><<<blocks, kSelWarps * 32, 0, st>>>(P);
-        if ((e = cudaGetLastError())) return e;
-        unsigned n_fb = 0;
-        if ((e = cudaMemcpyAsync(&n_fb, B.fbn.p, 4, cudaMemcpyDeviceToHost, st))) return e;
-        if ((e = cudaStreamSynchronize(st))) return e;
-        if (!n_fb) return cudaSuccess;
-        P.fallback = nullptr;
-        P.order = (const uint32_t *)B.fb.p;  // merge kernel on the unresolved hits
-        P.nq = n_fb;
-    }
+// Render mode keeps the merge kernel: hit records come in tracer order over a
+// strongly clustered traced map, where the collect-and-sort kernel's ball
+// sizing needs retries (measured 24.1 vs 20.4 ms per config-2 frame).
+cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st) {
+    if (P.nq == 0) return cudaSuccess;
     // persistent: enough warps to fill the SMs, grid-striding over the device-side hit count
     const unsigned blocks = (unsigned)std::min<size_t>((P.nq * 32 + 127) / 128, (size_t)sms * 16);
     const int kp = (P.K + 31) / 32;

@@ -78,7 +78,7 @@ cudaError_t knn_query(const KnnParams &P, cudaStream_t st);
 // K > 64: CTA-per-query select kernel + exact warp-kernel fallback (syncs the stream)
 cudaError_t knn_query_auto(KnnParams P, KnnBuffers &B, cudaStream_t st);
 // render mode: P.nq = upper bound on the hit count, grid-stride over *P.n_hits
-cudaError_t knn_query_render(const KnnParams &P, KnnBuffers &B, int sms, cudaStream_t st);
+cudaError_t knn_query_render(const KnnParams &P, int sms, cudaStream_t st);
 cudaError_t knn_order(const float *x3, const uint8_t *g, size_t n, KnnBuffers &B, const uint32_t **order,
                       cudaStream_t st);
 cudaError_t knn_make_queries(uint64_t initstate, uint64_t base, size_t batch, int n_phases,
