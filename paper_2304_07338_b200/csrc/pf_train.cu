@@ -35,8 +35,10 @@ namespace pfk {
 
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kChunk = 1024;  // queries per weight-gradient partial
+// 512 threads share one smem W^T image (134 KB for the paper field, one CTA
+// per SM) so an SM still runs 16 warps; 128 registers per thread fit.
+constexpr int kThreads = 512;
+constexpr int kChunk = 256;  // queries per weight-gradient partial
 
 __device__ __forceinline__ float relu(float x) { return x < 0.f ? 0.f : x; }
 
@@ -115,7 +117,7 @@ __device__ __forceinline__ void level_feats(const TrainParams &T, int lv, const 
 }
 
 template <int FP, int FD>
-__global__ void __launch_bounds__(kThreads) k_train_fwd(const TrainParams T, const float4 *img, int n4) {
+__global__ void __launch_bounds__(kThreads, 1) k_train_fwd(const TrainParams T, const float4 *img, int n4) {
     extern __shared__ float4 sm4[];
     load_image(img, n4, sm4);
     const float *sm = reinterpret_cast<const float *>(sm4);
@@ -217,7 +219,7 @@ __device__ __forceinline__ void level_scatter(const TrainParams &T, int lv, cons
 }
 
 template <int FP, int FD>
-__global__ void __launch_bounds__(kThreads) k_train_bwd(const TrainParams T, const float4 *img, int n4) {
+__global__ void __launch_bounds__(kThreads, 1) k_train_bwd(const TrainParams T, const float4 *img, int n4) {
     extern __shared__ float4 sm4[];
     load_image(img, n4, sm4);
     const float *sm = reinterpret_cast<const float *>(sm4);
