@@ -219,8 +219,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # smoke-testing the N > 1 logic on a 1-GPU box: PF_BENCH_ONE_DEVICE=1 puts
+    # every rank on cuda:0 and PF_DIST_BACKEND=gloo (NCCL refuses duplicate GPUs)
+    if os.environ.get("PF_BENCH_ONE_DEVICE") == "1":
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PF_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     if not (ROOT / "paper_2304_07338_b200" / "libpfgpu.so").exists():
         if rank == 0:
@@ -246,6 +254,29 @@ def main():
     per_shard = n_tiles_max * 16 * 16 * 3
     packed = torch.zeros(per_shard, dtype=torch.float32, device="cuda")
     gathered = torch.zeros(per_shard * world, dtype=torch.float32, device="cuda") if world > 1 else None
+    # N > 1 tile gather: "p2p" = every rank's compose kernel stores its tiles
+    # straight into rank 0's frame over NVLink (CUDA IPC mapping), fenced by a
+    # stream-ordered 1-element all-reduce; "nccl" = pack / all_gather / unpack.
+    gather = os.environ.get("PF_GATHER", "p2p") if world > 1 else "none"
+    sync = torch.zeros(1, dtype=torch.float32, device="cuda")
+    if gather == "p2p":
+        ok = 1
+        try:
+            obj = [None]
+            if rank == 0:
+                shared, obj[0] = ctx.ipc_frame_create(H_, W_)
+            dist.broadcast_object_list(obj, src=0)
+            if rank != 0:
+                shared = ctx.ipc_frame_open(obj[0], H_, W_)
+        except Exception as e:  # no IPC / peer access on this box: NCCL gather instead
+            print(f"rank {rank}: p2p gather unavailable ({e}); using NCCL", file=sys.stderr)
+            ok = 0
+        t = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            frame = shared
+        else:
+            gather = "nccl"
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     ctx.set_timing(True)
 
@@ -257,8 +288,12 @@ def main():
             ctx.set_medium(tf_i, 100.0)
             ctx.set_lights(li_i)
         frame_no[0] += 1
+        if gather == "p2p":
+            dist.all_reduce(sync)  # rank 0 is done with the previous frame
         st = ctx.render_neural(cam, rc, out=frame, stats=stats)
-        if world > 1:
+        if gather == "p2p":
+            dist.all_reduce(sync)  # every rank's tiles are in rank 0's frame
+        elif gather == "nccl":
             ctx.tiles_pack(cam, rc, frame, packed)
             dist.all_gather_into_tensor(gathered, packed)
             if rank == 0:
@@ -372,7 +407,7 @@ def main():
                                                  "(16x8 hash grid T=2^19, 5x64 MLP, random init)",
                        "mode": args.mode, "tiles": "16x16 interleaved over ranks",
                        "l2": "flushed (256 MiB write) between timed frames",
-                       "parallelism": f"tiles{world}"},
+                       "parallelism": f"tiles{world}", "gather": gather},
             "mrays_per_s": samples * world / (ms_per_step * 1e-3) / 1e6,
             "frame": {"samples": samples * world, "hits": hits, "hit_fraction": hits / max(samples, 1),
                       "steps_per_sample": steps_tot / max(samples, 1),
@@ -386,7 +421,7 @@ def main():
                          "peak_source": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) + (2 * args.steps if world > 1 else 0),
+            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) + (2 * args.steps if gather == "nccl" else 0),
             "clocks": clk.summary(),
             **extras,
         }

@@ -200,6 +200,17 @@ int pf_tiles_pack(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
 int pf_tiles_unpack(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
                     const float *packed_all, size_t per_shard_floats, float *frame_rgb);
 
+/* Tile gather over NVLink peer memory (CUDA IPC), the fused alternative to
+ * pack -> all_gather -> unpack: rank 0 allocates the frame and exports a
+ * 64-byte handle; every other rank maps it and passes the mapped pointer as
+ * out_rgb to pf_render_*, so its compose kernel stores its tiles straight
+ * into rank 0's frame.  A stream-ordered barrier (e.g. a 1-element NCCL
+ * all-reduce) after the render makes the frame complete on rank 0. */
+int pf_ipc_frame_create(pf_ctx *ctx, size_t bytes, void **dev_ptr, void *handle64);
+int pf_ipc_frame_open(pf_ctx *ctx, const void *handle64, void **dev_ptr);
+/* owner = 1 frees the allocation, 0 unmaps a peer mapping. */
+int pf_ipc_frame_release(pf_ctx *ctx, void *dev_ptr, int owner);
+
 /* ---- parity entry points: batched pf::delta_track / pf::transmittance --- */
 /* Ray i: origin o3[3i..], unit direction d3[3i..], [tmin, tmax]; its RNG is
  * make_rng(seed, stream, idx[i]).  hit[i] = 1/0, pos3 / rgba4 (may be NULL)

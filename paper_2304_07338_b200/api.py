@@ -208,6 +208,28 @@ def _n(x: Any) -> int:
     return int(x.shape[0])
 
 
+class _CudaFrame:
+    """__cuda_array_interface__ view of a library-owned device frame."""
+
+    def __init__(self, ptr: int, height: int, width: int, ctx, owner: bool):
+        self.ptr, self.shape, self.ctx, self.owner = ptr, (height, width, 3), ctx, owner
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+    def release(self):
+        if self.ptr:
+            lib().pf_ipc_frame_release(self.ctx._h, C.c_void_p(self.ptr), int(self.owner))
+            self.ptr = 0
+
+
+def _device_frame(ptr: int, height: int, width: int, ctx, owner: bool):
+    import torch
+    holder = _CudaFrame(ptr, height, width, ctx, owner)
+    t = torch.as_tensor(holder, device="cuda")
+    t._pf_holder = holder  # keeps the mapping alive with the tensor
+    return t
+
+
 # ------------------------------------------------------------- context ----
 
 
@@ -394,6 +416,19 @@ class Context:
         if stats:
             return out, {k: getattr(st, k) for k, _ in _lib.RenderStats._fields_}
         return out
+
+    # ---- multi-GPU frame over NVLink peer memory (CUDA IPC)
+    def ipc_frame_create(self, height: int, width: int):
+        """rank 0: a device frame other ranks can map; returns (tensor, 64-byte handle)."""
+        ptr, h = C.c_void_p(), (C.c_uint8 * 64)()
+        check(lib().pf_ipc_frame_create(self._h, height * width * 12, C.byref(ptr), h))
+        return _device_frame(ptr.value, height, width, self, owner=True), bytes(h)
+
+    def ipc_frame_open(self, handle: bytes, height: int, width: int):
+        """rank > 0: map rank 0's frame; renders with out= this tensor store into it."""
+        ptr, h = C.c_void_p(), (C.c_uint8 * 64).from_buffer_copy(handle)
+        check(lib().pf_ipc_frame_open(self._h, h, C.byref(ptr)))
+        return _device_frame(ptr.value, height, width, self, owner=False)
 
     def tiles_count(self, cam: _lib.Camera, cfg: RenderConfig, shard: int) -> int:
         n = C.c_int()

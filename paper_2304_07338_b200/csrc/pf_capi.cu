@@ -1519,4 +1519,39 @@ int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms
     return field_load(c, S.fd, (const float *)S.params.p, S.n_params);
 }
 
+// ----------------------------------------- multi-GPU frame over peer memory --
+int pf_ipc_frame_create(pf_ctx *c, size_t bytes, void **dev_ptr, void *handle64) {
+    if (!c || !dev_ptr || !handle64 || bytes == 0) return set_err(PF_ERR_INVALID, "pf_ipc_frame_create: bad argument");
+    PF_CUDA(cudaSetDevice(c->device));
+    void *p = nullptr;
+    PF_CUDA(cudaMalloc(&p, bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return set_err(PF_ERR_RUNTIME, "cudaIpcGetMemHandle failed: %s", cudaGetErrorString(e));
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    PF_CUDA(cudaMemset(p, 0, bytes));
+    *dev_ptr = p;
+    return PF_OK;
+}
+
+int pf_ipc_frame_open(pf_ctx *c, const void *handle64, void **dev_ptr) {
+    if (!c || !dev_ptr || !handle64) return set_err(PF_ERR_INVALID, "pf_ipc_frame_open: null argument");
+    PF_CUDA(cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    PF_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return PF_OK;
+}
+
+int pf_ipc_frame_release(pf_ctx *c, void *dev_ptr, int owner) {
+    if (!c || !dev_ptr) return set_err(PF_ERR_INVALID, "pf_ipc_frame_release: null argument");
+    PF_CUDA(cudaSetDevice(c->device));
+    PF_CUDA(owner ? cudaFree(dev_ptr) : cudaIpcCloseMemHandle(dev_ptr));
+    return PF_OK;
+}
+
 }  // extern "C"

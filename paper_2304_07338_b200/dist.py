@@ -11,6 +11,13 @@ index), hence the frame is byte-identical for any world size.  Per frame:
      the largest shard's tile count;
   3. one all_gather_into_tensor (NCCL over NVLink/NVSwitch) moves the packed
      tiles; rank 0 de-tiles them into the final frame (pf_tiles_unpack).
+The default device path (bench.py, render_frame_p2p) fuses the gather into
+the render instead: rank 0 exports its frame buffer (pf_ipc_frame_create,
+CUDA IPC), every other rank maps it (pf_ipc_frame_open) and renders with the
+mapped pointer as its output, so each rank's compose kernel stores its tiles
+straight into rank 0's frame over NVLink peer memory -- no pack, no
+collective payload, no unpack; a stream-ordered 1-element all-reduce before
+and after the render orders the frames.
 The functions below are the host-side statement of that tile map -- the CUDA
 kernels implement the same arithmetic -- and a CPU/gloo implementation of the
 exchange used to test the N > 1 logic without GPUs.
@@ -89,6 +96,30 @@ def render_frame_sharded(ctx, cam, rc, frame, packed, gathered, group=None):
     if rc.shard_index == 0:
         ctx.tiles_unpack(cam, rc, gathered, packed.numel(), frame)
     return frame
+
+
+def open_shared_frame(ctx, height, width, group=None):
+    """Rank 0 allocates + exports the frame, the other ranks map it (CUDA IPC)."""
+    import torch.distributed as dist
+    obj = [None]
+    frame = None
+    if dist.get_rank(group) == 0:
+        frame, obj[0] = ctx.ipc_frame_create(height, width)
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if frame is None:
+        frame = ctx.ipc_frame_open(obj[0], height, width)
+    return frame
+
+
+def render_frame_p2p(ctx, cam, rc, shared_frame, sync, group=None):
+    """Fused gather: this rank's compose kernel writes its tiles into rank 0's
+    frame (peer memory); the all-reduces order it against the previous frame's
+    readers and make the frame complete on rank 0."""
+    import torch.distributed as dist
+    dist.all_reduce(sync, group=group)
+    ctx.render_neural(cam, rc, out=shared_frame)
+    dist.all_reduce(sync, group=group)
+    return shared_frame
 
 
 def _check_cover(width, height, tile_w, tile_h, count) -> bool:
