@@ -527,6 +527,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParam
                 const float gx = gap(0, xl, xr);
                 n = 0;
                 bool over = false;
+                __syncwarp();  // the previous attempt's / query's buffer stores are ordered before ours
                 // rows of the cube in chunks of 32: each lane sizes one row (ball
                 // pruning, exact x-cell range through the binning function), a warp
                 // scan concatenates the row segments and all 32 lanes stream the
