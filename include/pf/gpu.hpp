@@ -150,7 +150,7 @@ class Device {
     }
     std::vector<double> train(const pf_train_desc &cfg, double *ms_knn = nullptr, double *ms_step = nullptr) {
         std::vector<double> hist(cfg.total_steps);
-        check(pf_train(ctx_, &cfg, hist.data(), ms_knn, ms_step));
+        check(pf_train(ctx_, &cfg, hist.data(), ms_knn, ms_step, nullptr, nullptr));
         return hist;
     }
 

@@ -330,8 +330,16 @@ typedef struct {
     double psi;                /* Eq. 7 precision */
     uint64_t seed;
 } pf_train_desc;
+/* ms_knn_steps / ms_step_steps (total_steps doubles each, may be NULL): the
+ * per-step split for the training log. */
 int pf_train(pf_ctx *ctx, const pf_train_desc *desc, double *loss_history, double *ms_knn,
-             double *ms_step);
+             double *ms_step, double *ms_knn_steps, double *ms_step_steps);
+/* Optimizer state (checkpoint / resume): master parameters and
+ * both Adam moments, n_params binary32 each, host or device memory; NULL
+ * skips one on get.  set also commits the parameters to the inference field.
+ * The Adam step counter is the caller's (pf_train_step's `step`). */
+int pf_train_state_get(pf_ctx *ctx, float *params, float *m, float *v, size_t n);
+int pf_train_state_set(pf_ctx *ctx, const float *params, const float *m, const float *v, size_t n);
 
 #ifdef __cplusplus
 }

@@ -138,7 +138,9 @@ _SIG = {
     "pf_train_counts": (C.c_int, [_P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "pf_train_params": (C.c_int, [_P, _P, C.c_size_t]),
     "pf_train_commit": (C.c_int, [_P]),
-    "pf_train": (C.c_int, [_P, C.POINTER(TrainDesc), _P, _P, _P]),
+    "pf_train": (C.c_int, [_P, C.POINTER(TrainDesc), _P, _P, _P, _P, _P]),
+    "pf_train_state_get": (C.c_int, [_P, _P, _P, _P, C.c_size_t]),
+    "pf_train_state_set": (C.c_int, [_P, _P, _P, _P, C.c_size_t]),
     "pf_ipc_frame_create": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_void_p), _P]),
     "pf_ipc_frame_open": (C.c_int, [_P, _P, C.POINTER(C.c_void_p)]),
     "pf_ipc_frame_release": (C.c_int, [_P, _P, C.c_int]),

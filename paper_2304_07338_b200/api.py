@@ -166,6 +166,76 @@ class TrainResult:
     loss_history: np.ndarray
     knn_ms: float       # cumulative make_batch (KNN + Eq. 6/7) device time
     step_ms: float      # cumulative train_step device time
+    knn_ms_steps: np.ndarray = None
+    step_ms_steps: np.ndarray = None
+    radius: np.ndarray = None
+    lr: np.ndarray = None
+
+    def write_log(self, path) -> None:
+        """Training log, one line per step: step, loss, radius, lr,
+        cumulative knn_time (ms), as comma-separated text."""
+        cum = np.cumsum(self.knn_ms_steps)
+        with open(path, "w") as f:
+            f.write("step,loss,radius,lr,knn_time_ms\n")
+            for i, l in enumerate(self.loss_history):
+                f.write(f"{i},{l:.17g},{self.radius[i]:.17g},{self.lr[i]:.17g},{cum[i]:.6f}\n")
+
+
+def lr_at(step: int, total: int, adam: "AdamConfig | None" = None) -> float:
+    """lr(step) = lr0 * decay^floor(max(0, step - decay_start * total) / interval) (SPEC.md:425)."""
+    a = adam or AdamConfig()
+    import math
+    return a.lr * a.decay ** math.floor(max(0.0, step - a.decay_start * total) / a.decay_interval)
+
+
+_CKPT_MAGIC = b"PFFC"
+
+
+def save_checkpoint(path, cfg: "FieldConfig", phase_set, step: int, params, m, v) -> None:
+    """Field checkpoint: header (configs, psi, G, next step), then the
+    flat parameter vector and both Adam moments, little-endian binary64."""
+    import struct
+    gs = np.asarray(phase_set, np.float64)
+    with open(path, "wb") as f:
+        f.write(_CKPT_MAGIC + struct.pack("<I", 1))
+        for hg in (cfg.pos, cfg.dir):
+            f.write(struct.pack("<iiiidi", hg.dims, hg.levels, hg.features, hg.base_res, float(hg.growth),
+                                hg.log2_table))
+        f.write(struct.pack("<iid", cfg.hidden_layers, cfg.width, float(cfg.psi)))
+        f.write(struct.pack("<I", len(gs)) + gs.astype("<f8").tobytes())
+        f.write(struct.pack("<QQ", int(step), len(params)))
+        for arr in (params, m, v):
+            f.write(np.asarray(arr, np.float64).astype("<f8").tobytes())
+
+
+def load_checkpoint(path):
+    """-> (FieldConfig, phase_set, next step, params, m, v) (binary64 arrays)."""
+    import struct
+    with open(path, "rb") as f:
+        buf = f.read()
+    if buf[:4] != _CKPT_MAGIC:
+        raise ValueError("field checkpoint: bad magic")
+    (ver,) = struct.unpack_from("<I", buf, 4)
+    if ver != 1:
+        raise ValueError(f"field checkpoint: unsupported version {ver}")
+    o = 8
+    grids = []
+    for _ in range(2):
+        d, lv, fe, br, gr, lt = struct.unpack_from("<iiiidi", buf, o)
+        o += struct.calcsize("<iiiidi")
+        grids.append(HashGrid(d, lv, fe, br, gr, lt))
+    hl, wd, psi = struct.unpack_from("<iid", buf, o)
+    o += struct.calcsize("<iid")
+    (ng,) = struct.unpack_from("<I", buf, o)
+    o += 4
+    gs = np.frombuffer(buf, "<f8", ng, o).copy()
+    o += 8 * ng
+    step, n = struct.unpack_from("<QQ", buf, o)
+    o += 16
+    arrs = [np.frombuffer(buf, "<f8", n, o + 8 * n * k).copy() for k in range(3)]
+    if o + 24 * n != len(buf):
+        raise ValueError("field checkpoint: truncated or oversized")
+    return FieldConfig(pos=grids[0], dir=grids[1], hidden_layers=hl, width=wd, psi=psi), list(gs), step, *arrs
 
 
 @dataclass
@@ -309,6 +379,7 @@ class Context:
         check(lib().pf_train_init(self._h, C.byref(cfg.c()), p, int(np.prod(keep.shape)),
                                   C.byref(adam.c()) if adam is not None else None))
         self.field_config = cfg
+        self.adam_config = adam
 
     def train_counts(self) -> tuple[int, int]:
         a, b = C.c_size_t(), C.c_size_t()
@@ -353,10 +424,37 @@ class Context:
         radii = np.ascontiguousarray(cfg.schedule_radii, np.float64)
         d = _lib.TrainDesc(int(cfg.total_steps), int(cfg.batch_size), int(cfg.K), len(ends), ends.ctypes.data,
                            radii.ctypes.data, float(cfg.psi), int(cfg.seed))
-        hist = np.zeros(int(cfg.total_steps), np.float64)
+        n = int(cfg.total_steps)
+        hist, ka, kb = np.zeros(n), np.zeros(n), np.zeros(n)
         a, b = C.c_double(), C.c_double()
-        check(lib().pf_train(self._h, C.byref(d), hist.ctypes.data, C.byref(a), C.byref(b)))
-        return TrainResult(hist, a.value, b.value)
+        check(lib().pf_train(self._h, C.byref(d), hist.ctypes.data, C.byref(a), C.byref(b), ka.ctypes.data,
+                             kb.ctypes.data))
+        radius = np.array([schedule_radius(cfg.schedule_ends, cfg.schedule_radii, s, n) for s in range(n)])
+        lrs = np.array([lr_at(s, n, getattr(self, "adam_config", None)) for s in range(n)])
+        return TrainResult(hist, a.value, b.value, ka, kb, radius, lrs)
+
+    def train_state(self):
+        """(params, m, v) of the optimizer, binary32."""
+        n_params, _ = self.train_counts()
+        out = [np.zeros(n_params, np.float32) for _ in range(3)]
+        check(lib().pf_train_state_get(self._h, *[o.ctypes.data for o in out], n_params))
+        return tuple(out)
+
+    def train_save(self, path, phase_set, next_step: int) -> None:
+        p, m, v = self.train_state()
+        save_checkpoint(path, self.field_config, phase_set, next_step, p, m, v)
+
+    def train_load(self, path, adam: "AdamConfig | None" = None):
+        """Restore a checkpoint bit-exactly (binary32 state stored as binary64);
+        returns (FieldConfig, phase_set, next step)."""
+        cfg, gs, step, p, m, v = load_checkpoint(path)
+        p32, m32, v32 = (np.ascontiguousarray(x, np.float32) for x in (p, m, v))
+        if not (np.array_equal(p32.astype(np.float64), p) and np.array_equal(m32.astype(np.float64), m)
+                and np.array_equal(v32.astype(np.float64), v)):
+            raise ValueError("field checkpoint: state is not binary32-representable")
+        self.train_init(cfg, p32, adam)
+        check(lib().pf_train_state_set(self._h, p32.ctypes.data, m32.ctypes.data, v32.ctypes.data, len(p32)))
+        return cfg, gs, step
 
     def field_query(self, x3, wsph2, g, decoded: bool = True, out=None):
         px, kx = _in(x3, np.float32)

@@ -1447,7 +1447,8 @@ int pf_train_commit(pf_ctx *c) {
     return field_load(c, c->train.fd, (const float *)c->train.params.p, c->train.n_params);
 }
 
-int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms_knn, double *ms_step) {
+int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms_knn, double *ms_step,
+             double *ms_knn_steps, double *ms_step_steps) {
     if (!c || !d) return set_err(PF_ERR_INVALID, "pf_train: null argument");
     if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train: call pf_train_init first");
     if (d->total_steps < 1 || d->batch < 1) return set_err(PF_ERR_INVALID, "TrainConfig: total_steps, batch >= 1");
@@ -1508,6 +1509,8 @@ int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms
         cudaEventElapsedTime(&b, ev[1], ev[2]);
         knn_ms += a;
         step_ms += b;
+        if (ms_knn_steps) ms_knn_steps[step] = a;
+        if (ms_step_steps) ms_step_steps[step] = b;
     }
     for (auto &e : ev) cudaEventDestroy(e);
     if (loss_history)
@@ -1517,6 +1520,31 @@ int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms
     if (ms_step) *ms_step = step_ms;
     // the renderer / field queries now use the trained field
     return field_load(c, S.fd, (const float *)S.params.p, S.n_params);
+}
+
+int pf_train_state_get(pf_ctx *c, float *params, float *m, float *v, size_t n) {
+    if (!c) return set_err(PF_ERR_INVALID, "null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train_state_get: call pf_train_init first");
+    if (n != c->train.n_params) return set_err(PF_ERR_INVALID, "pf_train_state_get: expected %zu", c->train.n_params);
+    PF_CUDA(cudaSetDevice(c->device));
+    const void *src[3] = {c->train.params.p, c->train.m.p, c->train.v.p};
+    float *dst[3] = {params, m, v};
+    for (int k = 0; k < 3; ++k)
+        if (dst[k]) PF_CUDA(cudaMemcpyAsync(dst[k], src[k], n * 4, cudaMemcpyDefault, c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
+    return PF_OK;
+}
+
+int pf_train_state_set(pf_ctx *c, const float *params, const float *m, const float *v, size_t n) {
+    if (!c || !params || !m || !v) return set_err(PF_ERR_INVALID, "pf_train_state_set: null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train_state_set: call pf_train_init first");
+    if (n != c->train.n_params) return set_err(PF_ERR_INVALID, "pf_train_state_set: expected %zu", c->train.n_params);
+    PF_CUDA(cudaSetDevice(c->device));
+    void *dst[3] = {c->train.params.p, c->train.m.p, c->train.v.p};
+    const float *src[3] = {params, m, v};
+    for (int k = 0; k < 3; ++k) PF_CUDA(cudaMemcpyAsync(dst[k], src[k], n * 4, cudaMemcpyDefault, c->stream));
+    PF_CUDA(cudaStreamSynchronize(c->stream));
+    return field_load(c, c->train.fd, (const float *)c->train.params.p, c->train.n_params);
 }
 
 // ----------------------------------------- multi-GPU frame over peer memory --

@@ -155,3 +155,41 @@ def test_staggered_schedule_is_cheaper(ctx, traced_map):
     print("final loss", ls, ln, "knn ms", s.knn_ms, n.knn_ms)
     assert s.knn_ms < n.knn_ms
     assert abs(ls - ln) <= 0.15 * max(ls, ln) or ls < ln
+
+
+def test_checkpoint_resume_is_bit_exact(ctx, tmp_path):
+    """a field checkpoint (params + Adam moments, binary64 on disk)
+    restores training bit-exactly."""
+    fc = FieldConfig.desk()
+    ctx.train_init(fc, fc.init_params(seed=11, embed_scale=0.1, bias_scale=0.05))
+    batches = [_batch(2048, 40 + s) for s in range(6)]
+    for s in range(3):
+        ctx.train_step(*batches[s], step=s, total_steps=6)
+    ckpt = tmp_path / "field.pffc"
+    ctx.train_save(ckpt, [-0.75, 0.0, 0.75], 3)
+    for s in range(3, 6):
+        ctx.train_step(*batches[s], step=s, total_steps=6)
+    a = ctx.train_state()
+    cfg, gs, nxt = ctx.train_load(ckpt)
+    assert cfg == fc and nxt == 3 and gs == [-0.75, 0.0, 0.75]
+    for s in range(nxt, 6):
+        ctx.train_step(*batches[s], step=s, total_steps=6)
+    b = ctx.train_state()
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+def test_training_log(ctx, traced_map, tmp_path):
+    """one line per step -- step, loss, radius, lr, cumulative knn_time."""
+    fc = FieldConfig.desk()
+    ctx.train_init(fc, fc.init_params(seed=3, embed_scale=1e-4, bias_scale=0.0))
+    res = ctx.train(TrainConfig(total_steps=40, batch_size=1024, K=32, schedule_ends=(0.5, 1.0),
+                                schedule_radii=(0.1, 0.2), seed=1))
+    log = tmp_path / "train.csv"
+    res.write_log(log)
+    rows = log.read_text().strip().splitlines()
+    assert rows[0] == "step,loss,radius,lr,knn_time_ms" and len(rows) == 41
+    cols = np.array([[float(v) for v in r.split(",")] for r in rows[1:]])
+    assert np.array_equal(cols[:, 0], np.arange(40))
+    assert set(cols[:, 2]) == {0.1, 0.2} and np.all(np.diff(cols[:, 4]) >= 0)
+    assert abs(res.knn_ms - res.knn_ms_steps.sum()) < 1e-6 * max(1.0, res.knn_ms)

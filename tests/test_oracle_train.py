@@ -93,3 +93,20 @@ def test_sparse_adam_only_touches_visited_entries(oracle):
     assert not np.any(changed & ~mask)
     assert np.all(q[n_tab:] != p[n_tab:]) or np.count_nonzero(grad[n_tab:] == 0) > 0
     assert loss > 0
+
+
+def test_checkpoint_file_roundtrip(tmp_path):
+    from paper_2304_07338_b200 import load_checkpoint, lr_at, save_checkpoint
+    fc = FieldConfig.desk()
+    p = fc.init_params(seed=2, embed_scale=0.2)
+    m, v = p * 0.5, np.abs(p) * 1e-3
+    f = tmp_path / "x.pffc"
+    save_checkpoint(f, fc, [-0.75, 0.0, 0.75], 12, p, m, v)
+    cfg, gs, step, p2, m2, v2 = load_checkpoint(f)
+    assert cfg == fc and gs == [-0.75, 0.0, 0.75] and step == 12
+    for a, b in ((p, p2), (m, m2), (v, v2)):
+        assert np.array_equal(a.astype(np.float64), b)
+    f.write_bytes(f.read_bytes()[:-8])
+    with pytest.raises(ValueError):
+        load_checkpoint(f)
+    assert [lr_at(s, 3000) for s in (0, 2125, 3000)] == pytest.approx([9e-4, 8.28e-4, 4.473055573e-5], rel=1e-9)
