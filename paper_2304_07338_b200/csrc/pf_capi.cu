@@ -160,7 +160,7 @@ struct pf_ctx {
     FieldHost fhost;
     DevBuf f_tables, f_img, f_feat;
     int f_nwg = 0;
-    size_t f_smem = 0;
+    size_t f_smem = 0, f_abytes = 32768;
     int sms = 0;
     // render scratch
     DevBuf slots, hits, hit_dir, counters, frame_stage, stage[8];
@@ -524,8 +524,8 @@ static int field_load(pf_ctx *c, const FieldDesc &f, const float *params, size_t
     field_pack(f, src, h);
     if ((int)h.levels.size() > PF_FIELD_MAX_LEVELS) return set_err(PF_ERR_INVALID, "too many levels");
     int nwg;
-    size_t smem;
-    if (field_launch_config(h, nwg, smem, c->device))
+    size_t smem, a_bytes;
+    if (field_launch_config(h, nwg, smem, a_bytes, c->device))
         return set_err(PF_ERR_INVALID, "pf_field_load: MLP does not fit in shared memory");
     PF_CUDA(c->f_tables.ensure(h.tables.size() * 2));
     PF_CUDA(c->f_img.ensure(h.image.size()));
@@ -537,6 +537,7 @@ static int field_load(pf_ctx *c, const FieldDesc &f, const float *params, size_t
     c->fhost = std::move(h);
     c->f_nwg = nwg;
     c->f_smem = smem;
+    c->f_abytes = a_bytes;
     c->has_field = true;
     return PF_OK;
 }
@@ -574,9 +575,9 @@ static FieldParams field_params(pf_ctx *c) {
     P.K0 = h.K0;
     P.hidden_layers = h.hidden_layers;
     P.n_wg = c->f_nwg;
-    P.tmem_cols = c->f_nwg <= 2 ? 128u : 256u;
+    P.tmem_cols = c->f_nwg <= 2 ? 128u : (c->f_nwg <= 4 ? 256u : 512u);
     P.img_bytes = (uint32_t)h.image.size();
-    P.a_bytes = 32768u;
+    P.a_bytes = (uint32_t)c->f_abytes;
     for (int i = 0; i < 8; ++i) P.off_w[i] = h.off_w[i];
     P.off_bias = h.off_bias;
     P.psi_log2_10 = (float)(h.psi * 3.3219280948873623478703194294894);

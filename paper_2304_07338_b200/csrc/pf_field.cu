@@ -20,6 +20,7 @@
 #include <cuda_fp16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -201,12 +202,16 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
 //   layers 1..H: tcgen05.ld -> bias + ReLU -> fp16 -> st.shared into the A
 //            tile -> next layer's MMA (N=16 for the 3-wide output layer);
 //   epilogue: Eq. 8 decode, compose term into the sample's slot.
-__global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
+__global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *img = smem;
     uint8_t *abase = smem + P.img_bytes;
     // barriers: [0] weights; per warpgroup w: 1+5w: full0, full1, empty0, empty1, done
-    uint64_t *bars = reinterpret_cast<uint64_t *>(abase + (size_t)P.n_wg * 32768);
+    // a_bytes per warpgroup: 32 KB = two chunk buffers (layer-0 double
+    // buffering), 16 KB = one (8 warpgroups per SM, layer-0 TMA latency hidden
+    // by the other warpgroups instead)
+    const int nb = P.a_bytes >= 32768u ? 2 : 1;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(abase + (size_t)P.n_wg * P.a_bytes);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + 5 * P.n_wg);
 
     const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5;
@@ -228,7 +233,8 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
     const size_t n_all = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
     const size_t n_items = n_all > P.row0 ? min(n_all - P.row0, P.row_cap) : 0;
     const size_t n_tiles = (n_items + 127) / 128;
-    const uint32_t buf_s[2] = {smem_u32(abase + (size_t)wg * 32768), smem_u32(abase + (size_t)wg * 32768 + 16384)};
+    const uint32_t buf_s[2] = {smem_u32(abase + (size_t)wg * P.a_bytes),
+                               smem_u32(abase + (size_t)wg * P.a_bytes + (nb == 2 ? 16384u : 0u))};
     const uint32_t img_s = smem_u32(img);
     const uint32_t tmem_wg = tmem_base + (uint32_t)(wg * 64);
     const uint32_t tmem_rows = tmem_wg + ((uint32_t)(32 * (warp & 3)) << 16);
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
         // ---- layer 0: TMA-fed chunks (only thread r == 0 drives the pipeline)
         if (r == 0) {
             auto load = [&](int j) {
-                const int b = j & 1;
+                const int b = j % nb;
                 if (empty_pending[b]) {
                     mbar_wait(empty[b], ph_empty[b]);
                     ph_empty[b] ^= 1u;
@@ -258,8 +264,8 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
             };
             load(0);
             for (int j = 0; j < P.nch; ++j) {
-                const int b = j & 1;
-                if (j + 1 < P.nch) load(j + 1);
+                const int b = j % nb;
+                if (nb == 2 && j + 1 < P.nch) load(j + 1);  // prefetch into the other buffer
                 mbar_wait(full[b], ph_full[b]);
                 ph_full[b] ^= 1u;
                 tc_fence_after();
@@ -272,6 +278,7 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
                 }
                 umma_commit(empty[b]);
                 empty_pending[b] = true;
+                if (nb == 1 && j + 1 < P.nch) load(j + 1);  // waits for this chunk's MMAs
             }
             umma_commit(done);
         }
@@ -289,22 +296,26 @@ __global__ void __launch_bounds__(512, 1) k_field_mlp(const FieldParams P) {
 
         // ---- hidden layers (epilogue of layer L-1 feeds the MMA of layer L)
         for (int L = 1; L <= P.hidden_layers; ++L) {
-            const int b = L & 1;
+            const int b = (L & 1) % nb;
             const float *bl = bias + (L - 1) * 64;
+            const uint32_t pa = buf_s[b] + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u;  // K=64: SBO 1024
+            // two halves of 32 columns: both 16-column loads of a half in flight, one wait
 #pragma unroll
-            uint32_t acc[64];  // all four 16-column loads in flight, one wait
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t acc[32];
+                tmem_ld16(tmem_rows + 32 * hf, acc);
+                tmem_ld16(tmem_rows + 32 * hf + 16, acc + 16);
+                tmem_ld_wait();
+                tmem_regs_ready<32>(acc);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld16(tmem_rows + 16 * c, acc + 16 * c);
-            tmem_ld_wait();
-            tmem_regs_ready<64>(acc);
+                for (int c = 0; c < 2; ++c) {
+                    const int col = 32 * hf + 16 * c;
+                    float a[16];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float a[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) a[i] = fmaxf(__uint_as_float(acc[16 * c + i]) + bl[16 * c + i], 0.f);
-                const uint32_t pa = buf_s[b] + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u;  // K=64: SBO 1024
-                store_feats<8>(pa, 0, 16 * c, 1024u, a);
-                store_feats<8>(pa, 0, 16 * c + 8, 1024u, a + 8);
+                    for (int i = 0; i < 16; ++i) a[i] = fmaxf(__uint_as_float(acc[16 * c + i]) + bl[col + i], 0.f);
+                    store_feats<8>(pa, 0, col, 1024u, a);
+                    store_feats<8>(pa, 0, col + 8, 1024u, a + 8);
+                }
             }
             tc_fence_before();
             fence_proxy_async_smem();
@@ -485,18 +496,28 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
     }
 }
 
-int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, int device) {
+int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_bytes, int device) {
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    const size_t per_wg = 32768;  // two 128 x 64 fp16 chunk tiles
-    const size_t fixed = h.image.size() + 256;
+    const size_t fixed = h.image.size() + 512;
+    // preferred: 8 warpgroups x one 16 KB tile (8 tiles in flight per SM, TMEM
+    // 8 x 64 columns); else up to 4 warpgroups x two 16 KB chunk buffers.
+    // PF_MLP_WG=4 forces the double-buffered 4-warpgroup layout (A/B).
+    const char *e = std::getenv("PF_MLP_WG");
+    const int want = e ? std::atoi(e) : 8;
     n_wg = 0;
-    for (int k = 4; k >= 1; --k)
-        if (fixed + k * per_wg <= (size_t)max_smem) {
-            n_wg = k;
-            break;
-        }
-    smem = fixed + (size_t)n_wg * per_wg;
+    if (want >= 8 && fixed + 8 * 16384 <= (size_t)max_smem) {
+        n_wg = 8;
+        a_bytes = 16384;
+    } else {
+        for (int k = 4; k >= 1; --k)
+            if (fixed + k * 32768 <= (size_t)max_smem) {
+                n_wg = k;
+                break;
+            }
+        a_bytes = 32768;
+    }
+    smem = fixed + (size_t)n_wg * a_bytes;
     return n_wg > 0 ? 0 : 1;
 }
 

@@ -75,7 +75,7 @@ size_t field_grid_param_count(const FieldGridDesc &g);
 size_t field_param_count(const FieldDesc &d);
 const char *field_validate(const FieldDesc &d);
 void field_pack(const FieldDesc &d, const float *params, FieldHost &out);
-int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, int device);
+int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_bytes, int device);
 // encode (grid-stride, full occupancy) + MLP (persistent, n_wg warpgroups)
 cudaError_t launch_field(const FieldParams &P, int fp, int fd, int grid, size_t smem,
                          cudaStream_t st);
