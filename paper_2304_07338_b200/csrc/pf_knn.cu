@@ -398,40 +398,47 @@ static bool knn_sel_disabled() {
 }
 constexpr int kSelCap = 256;
 
-// Warp bitonic sort of S*32 keys held as r[s] = element s*32 + lane:
-// strides >= 32 exchange registers, smaller strides exchange lanes.
+// Bitonic network stages for one k2 (block size of the current merge), strides
+// jstart .. 1, on S*32 keys held as r[s] = element base + s*32 + lane: strides
+// >= 32 exchange registers, smaller strides exchange lanes.  Directions come
+// from the GLOBAL element index, so warps can run their parts of a larger
+// network.
 template <int S>
-__device__ __forceinline__ void warp_sort_regs(uint64_t (&r)[S], unsigned lane) {
+__device__ __forceinline__ void warp_bitonic_stage(uint64_t (&r)[S], unsigned lane, int base, int k2, int jstart) {
 #pragma unroll
-    for (int k2 = 2; k2 <= S * 32; k2 <<= 1) {
+    for (int jj = jstart; jj > 0; jj >>= 1) {
+        if (jj >= 32) {
+            const int js = jj >> 5;
 #pragma unroll
-        for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
-            if (jj >= 32) {
-                const int js = jj >> 5;
+            for (int sI = 0; sI < S; ++sI) {
+                if (sI & js) continue;
+                const int i = base + sI * 32 + (int)lane;
+                const bool up = (i & k2) == 0;
+                const uint64_t a = r[sI], b = r[sI | js];
+                const bool sw = (a > b) == up;
+                r[sI] = sw ? b : a;
+                r[sI | js] = sw ? a : b;
+            }
+        } else {
 #pragma unroll
-                for (int sI = 0; sI < S; ++sI) {
-                    if (sI & js) continue;
-                    const int i = sI * 32 + (int)lane;
-                    const bool up = (i & k2) == 0;
-                    const uint64_t a = r[sI], b = r[sI | js];
-                    const bool sw = (a > b) == up;
-                    r[sI] = sw ? b : a;
-                    r[sI | js] = sw ? a : b;
-                }
-            } else {
-#pragma unroll
-                for (int sI = 0; sI < S; ++sI) {
-                    const int i = sI * 32 + (int)lane;
-                    const uint64_t o = __shfl_xor_sync(0xffffffffu, r[sI], jj);
-                    const bool lower = (lane & jj) == 0;
-                    const bool up = (i & k2) == 0;
-                    // lower element keeps min when ascending
-                    const bool take_min = lower == up;
-                    r[sI] = take_min ? (o < r[sI] ? o : r[sI]) : (o > r[sI] ? o : r[sI]);
-                }
+            for (int sI = 0; sI < S; ++sI) {
+                const int i = base + sI * 32 + (int)lane;
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, r[sI], jj);
+                const bool lower = (lane & jj) == 0;
+                const bool up = (i & k2) == 0;
+                // lower element keeps min when ascending
+                const bool take_min = lower == up;
+                r[sI] = take_min ? (o < r[sI] ? o : r[sI]) : (o > r[sI] ? o : r[sI]);
             }
         }
     }
+}
+
+// Warp bitonic sort of S*32 keys held as r[s] = element s*32 + lane.
+template <int S>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&r)[S], unsigned lane) {
+#pragma unroll
+    for (int k2 = 2; k2 <= S * 32; k2 <<= 1) warp_bitonic_stage<S>(r, lane, 0, k2, k2 >> 1);
 }
 
 template <int S>
@@ -704,6 +711,46 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParam
 // Exactness: every photon with d2 <= rho^2 is collected, so when >= K are
 // found the K smallest keys of the whole phase are among them.
 constexpr int kCtaThreads = 256;
+
+// Block bitonic sort of P2 keys (power of two, 256..1024) in shared memory:
+// every warp sorts its 128-key run in registers, then each merge level does
+// its strides >= 128 in shared memory (block barriers) and its strides < 128
+// in registers again -- 6 barrier stages for 1024 keys instead of 55.
+__device__ __forceinline__ void cta_sort(uint64_t *a, int P2, int warp, unsigned lane, int tid) {
+    const bool act = warp < P2 / 128;
+    const int base = warp * 128;
+    uint64_t r[4];
+    if (act) {
+#pragma unroll
+        for (int sI = 0; sI < 4; ++sI) r[sI] = a[base + sI * 32 + (int)lane];
+#pragma unroll
+        for (int k2 = 2; k2 <= 128; k2 <<= 1) warp_bitonic_stage<4>(r, lane, base, k2, k2 >> 1);
+#pragma unroll
+        for (int sI = 0; sI < 4; ++sI) a[base + sI * 32 + (int)lane] = r[sI];
+    }
+    __syncthreads();
+    for (int k2 = 256; k2 <= P2; k2 <<= 1) {
+        for (int jj = k2 >> 1; jj >= 128; jj >>= 1) {
+            for (int pI = tid; pI < P2 / 2; pI += kCtaThreads) {
+                const int i = (pI / jj) * 2 * jj + (pI % jj), ij = i + jj;
+                const uint64_t x = a[i], y = a[ij];
+                if ((x > y) == ((i & k2) == 0)) {
+                    a[i] = y;
+                    a[ij] = x;
+                }
+            }
+            __syncthreads();
+        }
+        if (act) {
+#pragma unroll
+            for (int sI = 0; sI < 4; ++sI) r[sI] = a[base + sI * 32 + (int)lane];
+            warp_bitonic_stage<4>(r, lane, base, k2, 64);
+#pragma unroll
+            for (int sI = 0; sI < 4; ++sI) a[base + sI * 32 + (int)lane] = r[sI];
+        }
+        __syncthreads();
+    }
+}
 constexpr int kCtaCap = 4608;  // collected keys per query (36 KB)
 
 __global__ void __launch_bounds__(kCtaThreads) k_knn_query_cta(const KnnParams P) {
@@ -897,25 +944,20 @@ __global__ void __launch_bounds__(kCtaThreads) k_knn_query_cta(const KnnParams P
                 for (int i = tid; i < n; i += kCtaThreads)
                     if (keys[i] <= kth) sel[atomicAdd(&s_cnt, 1)] = keys[i];
                 __syncthreads();
-                int P2 = 1;
+                int P2 = 32;
                 while (P2 < count) P2 <<= 1;
                 for (int i = count + tid; i < P2; i += kCtaThreads) sel[i] = ~0ull;
                 __syncthreads();
-                for (int k2 = 2; k2 <= P2; k2 <<= 1)
-                    for (int j = k2 >> 1; j > 0; j >>= 1) {
-                        for (int i = tid; i < P2; i += kCtaThreads) {
-                            const int ij = i ^ j;
-                            if (ij > i) {
-                                const uint64_t a = sel[i], b = sel[ij];
-                                const bool up = (i & k2) == 0;
-                                if ((a > b) == up) {
-                                    sel[i] = b;
-                                    sel[ij] = a;
-                                }
-                            }
-                        }
-                        __syncthreads();
+                if (P2 >= 256) {
+                    cta_sort(sel, P2, warp, lane, tid);
+                } else {
+                    if (warp == 0) {
+                        if (P2 == 32) sort_buf<1>(sel, count, lane);
+                        else if (P2 == 64) sort_buf<2>(sel, count, lane);
+                        else sort_buf<4>(sel, count, lane);
                     }
+                    __syncthreads();
+                }
                 break;
             }
         }
