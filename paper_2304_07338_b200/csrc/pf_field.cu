@@ -282,7 +282,9 @@ __global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
             }
             umma_commit(done);
         }
-        mbar_wait(done, ph_done);
+        // one warp polls the mbarrier, the other three sleep in the named barrier
+        if ((r >> 5) == 0) mbar_wait(done, ph_done);
+        named_bar_sync(1 + wg, 128);
         ph_done ^= 1u;
         tc_fence_after();
         if (r == 0) {  // keep the per-buffer parities in step (both are complete by now)
@@ -325,7 +327,8 @@ __global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
                 issue_layer(buf_s[b], img_s + P.off_w[L], 64, L < P.hidden_layers ? 64 : 16, tmem_wg);
                 umma_commit(done);
             }
-            mbar_wait(done, ph_done);
+            if ((r >> 5) == 0) mbar_wait(done, ph_done);
+            named_bar_sync(1 + wg, 128);
             ph_done ^= 1u;
             tc_fence_after();
         }
