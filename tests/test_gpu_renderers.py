@@ -191,3 +191,31 @@ def test_photon_map_empty_map_is_direct_light(ctx):
         a = ctx.render_photon_map(cam, RenderConfig(spp=2, g=0.75, seed=4, mode=mode), K=16)
         b = ctx.render_neural(cam, RenderConfig(spp=2, g=0.75, seed=4, mode=mode, use_field=False))
         assert np.array_equal(a, b)
+
+
+def test_two_lights_three_trials_parity(ctx, oracle):
+    """The per-light NEE loop with n_trials > 1 (transmittance's trial loop,
+    volume.cpp:240-255) in every renderer, against the oracle."""
+    vol = synth_volume("sphere_sinusoid", 32)
+    tf = tf_scene_b()
+    lights = np.array([[2.0, 2.5, -1.0, 1.0, 0.8, 0.6], [-1.0, 0.5, 0.5, 0.3, 0.5, 1.0]])
+    ctx.upload_volume(vol)
+    ctx.set_medium(tf, 100.0)
+    ctx.set_lights(lights)
+    ph = synth_photons(8000, 3, seed=9)
+    ph["power"] *= 1e-3
+    ctx.knn_build(ph, PHASES)
+    osc = oracle.OracleScene(vol, tf, 100.0)
+    cam = CameraSpec(40, 30)
+    rc = RenderConfig(spp=2, g=-0.75, seed=13, mode="parity", nee_trials=3, background=(0.1, 0.1, 0.1))
+    pt = PathTraceConfig(max_bounces=6)
+    got = ctx.render_path_traced(cam, rc, pt)
+    ref, _ = oracle.render_path_traced(osc, lights, cam, rc, pt)
+    assert _rel_mismatch(got, ref) <= 0.01 * 40 * 30
+    got = ctx.render_photon_map(cam, rc, K=16, r_max=0.2)
+    ref, _ = oracle.render_photon_map(osc, lights, ph, 0, 16, 0.2, cam, rc)
+    assert _rel_mismatch(got, ref, 1e-12) <= 3
+    rc2 = RenderConfig(spp=2, g=-0.75, seed=13, mode="parity", nee_trials=3, use_field=False)
+    got = ctx.render_neural(cam, rc2)
+    ref, _ = oracle.render_neural(osc, lights, None, None, cam, rc2)
+    assert _rel_mismatch(got, ref, 1e-12) <= 3
