@@ -339,11 +339,13 @@ def main():
     peaks, peak_kind = load_peaks()
     hbm = float(peaks["hbm_gbs"])
     achieved = steps_tot * 32.0 / (tr_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = sm_issue = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get("k_render_trace_fast" if args.mode == "fast"
-                                                    else "k_render_trace_parity")
+        tj = json.loads(tfile.read_text())
+        kname = "k_render_trace_fast" if args.mode == "fast" else "k_render_trace_parity"
+        traffic = tj.get(kname)
+        sm_issue = tj.get("sm_throughput_pct", {}).get(kname)
 
     # ---- e2e: public API with host buffers (per-frame TF/light/camera in, frame out)
     e2e = None
@@ -418,7 +420,11 @@ def main():
                          "frac": achieved / hbm, "traffic": traffic,
                          "per_unit": "32 B (8 x f32 voxels) per tentative collision, "
                                      f"{steps_tot:.3g} collisions per launch",
-                         "peak_source": peak_kind},
+                         "peak_source": peak_kind,
+                         # the macro-cell majorants remove ~97% of the reference's tentative
+                         # collisions, so the kernel is issue/latency-bound, not HBM-bound:
+                         # ncu's SM throughput (% of peak) for it, from profiles/ (cold cache)
+                         "sm_throughput_pct_ncu": sm_issue},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) + (2 * args.steps if gather == "nccl" else 0),
