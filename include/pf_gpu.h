@@ -168,6 +168,14 @@ int pf_camera_make(const double pos[3], const double look_at[3], const double up
  * pixels of other shards are left untouched.  stats may be NULL. */
 int pf_render_neural(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc,
                      float *out_rgb, pf_render_stats *stats);
+/* Pipelined frames into HOST memory: enqueue the frame and return at once; the
+ * device->host copy of out_rgb (pinned memory for real overlap) runs on the
+ * context's copy stream while the next frame's kernels run (two frames in
+ * flight, double-buffered device staging).  out_rgb is complete after
+ * pf_frame_wait(ctx, out_rgb) or pf_ctx_synchronize. */
+int pf_render_neural_async(pf_ctx *ctx, const pf_camera *cam, const pf_render_desc *desc, float *host_out);
+int pf_frame_wait(pf_ctx *ctx, const float *host_out);
+
 /* ---- the comparison renderers of SPEC.md render module ------------------ */
 /* render_path_traced(scene, camera, spp, max_bounces, rng):
  * the volumetric path tracer with NEE at every vertex, HG-sampled

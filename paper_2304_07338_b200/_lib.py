@@ -144,6 +144,8 @@ _SIG = {
     "pf_ipc_frame_create": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_void_p), _P]),
     "pf_ipc_frame_open": (C.c_int, [_P, _P, C.POINTER(C.c_void_p)]),
     "pf_ipc_frame_release": (C.c_int, [_P, _P, C.c_int]),
+    "pf_render_neural_async": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), _P]),
+    "pf_frame_wait": (C.c_int, [_P, _P]),
 }
 EXPORTS = tuple(_SIG)
 

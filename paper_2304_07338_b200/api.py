@@ -488,6 +488,19 @@ class Context:
             return out, {k: getattr(st, k) for k, _ in _lib.RenderStats._fields_}
         return out
 
+    def render_neural_async(self, cam: _lib.Camera | CameraSpec, cfg: RenderConfig, out):
+        """Enqueue a frame into HOST memory `out` (pinned for overlap) and return;
+        `out` is complete after frame_wait(out) / synchronize()."""
+        if isinstance(cam, CameraSpec):
+            cam = self.camera(cam)
+        po, out = _out(out, (cam.height, cam.width, 3), np.float32)
+        check(lib().pf_render_neural_async(self._h, C.byref(cam), C.byref(cfg.c()), po))
+        return out
+
+    def frame_wait(self, out) -> None:
+        po, _ = _out(out, None, np.float32)
+        check(lib().pf_frame_wait(self._h, po))
+
     def render_path_traced(self, cam: _lib.Camera | CameraSpec, cfg: RenderConfig,
                            path: PathTraceConfig | None = None, out=None, stats: bool = False):
         """render_path_traced: NEE at every vertex, HG continuation."""

@@ -172,6 +172,13 @@ struct pf_ctx {
     size_t k_n = 0;
     // photon trace (Alg. 1): resident result + scratch
     DevBuf t_rec, t_rec_photon, t_counts, t_offs, t_tmp, t_out, t_ctr;
+    // asynchronous host-output frames: double-buffered device staging, D2H on a
+    // copy stream overlapped with the next frame's kernels
+    cudaStream_t cstream = nullptr;
+    DevBuf aframe[2];
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+    const void *a_host[2] = {nullptr, nullptr};
+    int a_next = 0;
     // field training
     TrainState train;
     DevBuf tr_x, tr_w2, tr_g, tr_t, tr_w3, tr_gi, tr_t3d;
@@ -292,6 +299,14 @@ void pf_ctx_destroy(pf_ctx *c) {
     c->free_volume();
     for (auto &ev : c->ev)
         if (ev) cudaEventDestroy(ev);
+    if (c->cstream) {
+        cudaStreamSynchronize(c->cstream);
+        cudaStreamDestroy(c->cstream);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (c->ev_ready[k]) cudaEventDestroy(c->ev_ready[k]);
+        if (c->ev_copied[k]) cudaEventDestroy(c->ev_copied[k]);
+    }
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -314,8 +329,10 @@ int pf_ctx_set_stream(pf_ctx *c, void *s) {
 }
 
 int pf_ctx_synchronize(pf_ctx *c) {
-    if (!c) return set_err(PF_ERR_INVALID, "null context");
+    if (!c) return set_err(PF_ERR_INVALID, "null argument");
+    PF_CUDA(cudaSetDevice(c->device));
     PF_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->cstream) PF_CUDA(cudaStreamSynchronize(c->cstream));
     return PF_OK;
 }
 
@@ -879,6 +896,48 @@ int pf_render_path_traced(pf_ctx *c, const pf_camera *cam, const pf_render_desc 
 int pf_render_photon_map(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, int K, float r_max,
                          float *out_rgb, pf_render_stats *stats) {
     return render_common(c, cam, d, kLiPhotonMap, nullptr, K, r_max, out_rgb, stats);
+}
+
+int pf_render_neural_async(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, float *host_out) {
+    if (!c || !cam || !d || !host_out) return set_err(PF_ERR_INVALID, "pf_render_neural_async: null argument");
+    if (is_device_ptr(host_out)) return set_err(PF_ERR_INVALID, "pf_render_neural_async: host output expected");
+    PF_CUDA(cudaSetDevice(c->device));
+    if (!c->cstream) {
+        PF_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            PF_CUDA(cudaEventCreateWithFlags(&c->ev_ready[k], cudaEventDisableTiming));
+            PF_CUDA(cudaEventCreateWithFlags(&c->ev_copied[k], cudaEventDisableTiming));
+            PF_CUDA(cudaEventRecord(c->ev_copied[k], c->cstream));
+        }
+    }
+    const int k = c->a_next;
+    const size_t bytes = (size_t)cam->width * cam->height * 12;
+    // staging buffer k is free once its previous frame has been copied out
+    PF_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[k], 0));
+    if (c->aframe[k].cap < bytes) {
+        PF_CUDA(cudaStreamSynchronize(c->stream));
+        PF_CUDA(c->aframe[k].ensure(bytes));
+    }
+    if (d->shard_count > 1) PF_CUDA(cudaMemsetAsync(c->aframe[k].p, 0, bytes, c->stream));
+    if (int e = pf_render_neural(c, cam, d, (float *)c->aframe[k].p, nullptr)) return e;
+    PF_CUDA(cudaEventRecord(c->ev_ready[k], c->stream));
+    PF_CUDA(cudaStreamWaitEvent(c->cstream, c->ev_ready[k], 0));
+    PF_CUDA(cudaMemcpyAsync(host_out, c->aframe[k].p, bytes, cudaMemcpyDeviceToHost, c->cstream));
+    PF_CUDA(cudaEventRecord(c->ev_copied[k], c->cstream));
+    c->a_host[k] = host_out;
+    c->a_next = k ^ 1;
+    return PF_OK;
+}
+
+int pf_frame_wait(pf_ctx *c, const float *host_out) {
+    if (!c || !host_out) return set_err(PF_ERR_INVALID, "pf_frame_wait: null argument");
+    PF_CUDA(cudaSetDevice(c->device));
+    for (int k = 0; k < 2; ++k)
+        if (c->a_host[k] == host_out) {
+            PF_CUDA(cudaEventSynchronize(c->ev_copied[k]));
+            return PF_OK;
+        }
+    return set_err(PF_ERR_INVALID, "pf_frame_wait: no frame in flight for this buffer");
 }
 
 int pf_tiles_pack(pf_ctx *c, const pf_camera *cam, const pf_render_desc *d, const float *frame, float *packed) {

@@ -97,3 +97,31 @@ def test_render_background_only_outside_volume(scene):
     img, st = scene.render_neural(CameraSpec(32, 32, (0.5, 0.5, -0.9), (0.5, 0.5, -2.0), (0, 1, 0), 30.0),
                                   RenderConfig(spp=4, background=(0.25, 0.5, 0.75), use_field=False), stats=True)
     assert st["hits"] == 0 and np.all(img == np.array([0.25, 0.5, 0.75], np.float32))
+
+
+def test_async_host_frames_equal_sync(ctx):
+    """pf_render_neural_async: pipelined host frames equal the synchronous API's."""
+    import torch
+    from paper_2304_07338_b200 import FieldConfig, RenderConfig
+    from paper_2304_07338_b200.scene import CameraSpec, default_lights, synth_volume, tf_scene_b
+    ctx.upload_volume(synth_volume("sphere_sinusoid", 32))
+    ctx.set_medium(tf_scene_b(), 100.0)
+    ctx.set_lights(default_lights())
+    fc = FieldConfig.desk()
+    ctx.load_field(fc, fc.init_params(seed=3, embed_scale=0.3, bias_scale=0.1))
+    cam = CameraSpec(64, 40)
+    cfgs = [RenderConfig(spp=2, seed=s, mode=m) for s, m in [(1, "fast"), (2, "parity"), (3, "fast"), (4, "fast")]]
+    want = [ctx.render_neural(cam, c) for c in cfgs]
+    bufs = [torch.zeros((40, 64, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+    got = []
+    for i, c in enumerate(cfgs):
+        ctx.render_neural_async(cam, c, bufs[i % 2].numpy())
+        if i > 0:
+            ctx.frame_wait(bufs[(i - 1) % 2].numpy())
+            got.append(bufs[(i - 1) % 2].numpy().copy())
+    ctx.frame_wait(bufs[(len(cfgs) - 1) % 2].numpy())
+    got.append(bufs[(len(cfgs) - 1) % 2].numpy().copy())
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+    with pytest.raises(ValueError):
+        ctx.frame_wait(np.zeros((40, 64, 3), np.float32))
