@@ -1,4 +1,5 @@
-"""A/B of the tcgen05 MLP layouts (PF_MLP_WG, read at field load): frame field time + field microbench."""
+"""A/B of field-path knobs (argv[2], default PF_MLP_WG; e.g. PF_FIELD_FUSED): frame field time +
+field microbench + output equality."""
 import json
 import os
 import sys
@@ -7,6 +8,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_2304_07338_b200 import Context, FieldConfig, RenderConfig  # noqa: E402
+
+VAR = sys.argv[2] if len(sys.argv) > 2 else "PF_MLP_WG"
 
 if __name__ == "__main__":
     import numpy as np
@@ -32,7 +35,7 @@ if __name__ == "__main__":
         outs = {}
         for rep in range(2):
             for v in sys.argv[1].split(","):
-                os.environ["PF_MLP_WG"] = v
+                os.environ[VAR] = v
                 ctx.load_field(fc, prm)
                 sts = [ctx.render_neural(cam, rc, out=frame, stats=True)[1] for _ in range(8)][3:]
                 for _ in range(2):
