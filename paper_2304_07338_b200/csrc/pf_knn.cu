@@ -456,7 +456,7 @@ __device__ __forceinline__ void sort_buf(uint64_t *buf, int n, unsigned lane) {
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kSelWarps * 32) k_knn_query_sel(const KnnParams P) {
+__global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnParams P) {
     __shared__ uint64_t s_keys[kSelWarps][kSelCap];
     const unsigned lane = threadIdx.x & 31u;
     const int wi = threadIdx.x >> 5;
