@@ -27,7 +27,7 @@
 namespace pfk {
 
 template <bool PAR>
-__global__ void __launch_bounds__(PF_TRACE_THREADS) k_render_pt(const DevScene S, const TraceParams P) {
+__global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(const DevScene S, const TraceParams P) {
     using R = typename Prec<PAR>::R;
     R *slots = reinterpret_cast<R *>(P.slots);
     const R inv_sm = inv_majorant(S, R(0));
