@@ -146,7 +146,7 @@ struct pf_ctx {
     int atlas_log2 = 0;
     int mc[3] = {0, 0, 0};
     int macro = macro_default();  // voxels per macro-cell edge
-    DevBuf macro_mm, maj;
+    DevBuf macro_mm, maj, occ;
     int nx = 0, ny = 0, nz = 0;
     float vmin = 0.f, vmax = 0.f;
     // medium / lights
@@ -214,6 +214,7 @@ struct pf_ctx {
         S.atlas = vol_tex;
         S.atlas_log2 = atlas_log2;
         S.maj = (const float *)maj.p;
+        S.occ = (const int *)occ.p;
         for (int a = 0; a < 3; ++a) {
             const int n = a == 0 ? nx : a == 1 ? ny : nz;
             S.mc[a] = mc[a];
@@ -451,8 +452,9 @@ int pf_medium_set(pf_ctx *c, const double *tf_pts, int n_pts, double density_sca
     TfPoints tp;
     std::memset(&tp, 0, sizeof(tp));
     std::memcpy(tp.p, c->tf.data(), c->tf.size() * sizeof(double));
+    PF_CUDA(c->occ.ensure(6 * sizeof(int)));
     PF_CUDA(launch_macro_majorant((const float2 *)c->macro_mm.p, (size_t)c->mc[0] * c->mc[1] * c->mc[2], tp, n_pts,
-                                  density_scale, (float *)c->maj.p, c->stream));
+                                  density_scale, (float *)c->maj.p, c->mc[0], c->mc[1], (int *)c->occ.p, c->stream));
     c->has_medium = true;
     return PF_OK;
 }

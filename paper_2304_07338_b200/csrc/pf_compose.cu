@@ -133,7 +133,8 @@ __device__ double tf_alpha_host_like(const TfPoints &T, int n, double s) {
     return p[(hi - 1) * 5 + 4] + (p[hi * 5 + 4] - p[(hi - 1) * 5 + 4]) * t;
 }
 
-__global__ void k_macro_majorant(const float2 *mm, size_t ncells, const TfPoints T, int n, double ds, float *maj) {
+__global__ void k_macro_majorant(const float2 *mm, size_t ncells, const TfPoints T, int n, double ds, float *maj,
+                                 int mcx, int mcy, int *occ) {
     const double *tf = T.p;
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncells) return;
@@ -142,6 +143,16 @@ __global__ void k_macro_majorant(const float2 *mm, size_t ncells, const TfPoints
     for (int i = 0; i < n; ++i)
         if (tf[5 * i] > lo && tf[5 * i] < hi) m = fmax(m, tf[5 * i + 4]);
     maj[c] = m > 0.0 ? (float)(ds * m * (1.0 + 1e-5)) : 0.0f;
+    if (m > 0.0) {  // occupied-cell bounding box
+        const int cx = (int)(c % (size_t)mcx), cy = (int)((c / (size_t)mcx) % (size_t)mcy),
+                  cz = (int)(c / ((size_t)mcx * (size_t)mcy));
+        atomicMin(&occ[0], cx);
+        atomicMin(&occ[1], cy);
+        atomicMin(&occ[2], cz);
+        atomicMax(&occ[3], cx);
+        atomicMax(&occ[4], cy);
+        atomicMax(&occ[5], cz);
+    }
 }
 
 cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2 *mm, int mcx, int mcy, int mcz,
@@ -152,8 +163,12 @@ cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2
 }
 
 cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const TfPoints &tf_pts, int n_tf, double ds,
-                                  float *maj, cudaStream_t st) {
-    k_macro_majorant<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(mm, ncells, tf_pts, n_tf, ds, maj);
+                                  float *maj, int mcx, int mcy, int *occ, cudaStream_t st) {
+    // occ = {INT_MAX-ish x3, -1 x3} before the min / max reduction
+    cudaError_t e = cudaMemsetAsync(occ, 0x7f, 3 * sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(occ + 3, 0xff, 3 * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    k_macro_majorant<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(mm, ncells, tf_pts, n_tf, ds, maj, mcx, mcy, occ);
     return cudaGetLastError();
 }
 

@@ -83,6 +83,30 @@ __device__ __forceinline__ bool dda_advance(const DevScene &S, Dda &D, float &t,
     }
 }
 
+// Clip a flight [t0, t1] to the occupied-cell box (slightly expanded so
+// rounding can never cut off an occupied cell).  False: the flight only
+// crosses empty cells (sigma = 0), i.e. it passes unattenuated.
+__device__ __forceinline__ bool occ_clip(const DevScene &S, const float o[3], const float d[3], float &t0, float &t1) {
+    const int lo_x = __ldg(S.occ), hi_x = __ldg(S.occ + 3);
+    if (hi_x < lo_x) return false;  // no occupied cell at all
+    const int lo_c[3] = {lo_x, __ldg(S.occ + 1), __ldg(S.occ + 2)};
+    const int hi_c[3] = {hi_x, __ldg(S.occ + 4), __ldg(S.occ + 5)};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float lo = (float)lo_c[a] * S.mh[a] - 1e-4f, hi = (float)(hi_c[a] + 1) * S.mh[a] + 1e-4f;
+        const float inv = 1.0f / d[a];
+        float tn = (lo - o[a]) * inv, tf = (hi - o[a]) * inv;
+        if (inv < 0.0f) {
+            const float x = tn;
+            tn = tf;
+            tf = x;
+        }
+        t0 = fmaxf(t0, tn);
+        t1 = fminf(t1, tf);
+    }
+    return t0 <= t1;
+}
+
 __device__ __forceinline__ float sample_tau(Pcg &r) { return -__logf(pcg_one_minus_u_f(r)); }
 
 }  // namespace pfk

@@ -50,6 +50,10 @@ struct DevScene {
     // max_alpha, volume.cpp:163-168), so delta / ratio tracking against it is
     // unbiased; empty cells are skipped without a texture fetch.
     const float *maj;
+    // FAST mode: bounding box of the macro cells with a nonzero majorant
+    // (min cell x,y,z, max cell x,y,z; max < min when the medium is empty).
+    // sigma(x) = 0 outside it, so flights are clipped to it exactly.
+    const int *occ;
     int mc[3];
     float mh[3], minv_h[3];
 };

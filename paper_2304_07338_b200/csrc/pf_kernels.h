@@ -103,7 +103,7 @@ struct TfPoints {
     double p[16 * 5];
 };
 cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const TfPoints &tf_pts, int n_tf,
-                                  double density_scale, float *maj, cudaStream_t st);
+                                  double density_scale, float *maj, int mcx, int mcy, int *occ, cudaStream_t st);
 cudaError_t launch_build_atlas(const float *vol, int nx, int ny, int nz, int log2_cols, float *atlas,
                                size_t aw, size_t ah, cudaStream_t st);
 

@@ -53,6 +53,9 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
     auto start_flight = [&](R tmin, R tmax) -> bool {
         R a0, a1;
         if (!aabb_unit<R>(o, d, tmin, tmax, a0, a1) || !(sm > R(0))) return false;
+        if constexpr (!PAR) {
+            if (!occ_clip(S, o, d, a0, a1)) return false;  // only empty cells: no collision
+        }
         t = a0;
         t1 = a1;
         if constexpr (!PAR) {

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
                 wo[a] = -d[a];
             }
             float t0;
-            if (!aabb_unit<float>(o, d, 0.0f, __int_as_float(0x7f800000), t0, t1) || !(S.sigma_max_f > 0.0f)) {
+            if (!aabb_unit<float>(o, d, 0.0f, __int_as_float(0x7f800000), t0, t1) || !(S.sigma_max_f > 0.0f) ||
+                !occ_clip(S, o, d, t0, t1)) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = (float)P.bg[c];
                 continue;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
 #pragma unroll
                 for (int a = 0; a < 3; ++a) d[a] = dv[a] / len;
                 float a0, a1;
-                if (aabb_unit<float>(o, d, 0.0f, len, a0, a1) && S.sigma_max_f > 0.0f) {
+                if (aabb_unit<float>(o, d, 0.0f, len, a0, a1) && S.sigma_max_f > 0.0f && occ_clip(S, o, d, a0, a1)) {
                     t = a0;
                     t1 = a1;
                     T = 1.f;
@@ -189,7 +190,9 @@ __global__ void k_delta_track_batch_dda(const DevScene S, BatchParams B) {
     }
     float t, t1;
     B.hit[i] = 0;
-    if (!aabb_unit<float>(o, d, (float)B.tmin[i], (float)B.tmax[i], t, t1) || !(S.sigma_max_f > 0.f)) return;
+    if (!aabb_unit<float>(o, d, (float)B.tmin[i], (float)B.tmax[i], t, t1) || !(S.sigma_max_f > 0.f) ||
+        !occ_clip(S, o, d, t, t1))
+        return;
     Dda D;
     dda_init(S, o, d, t, D);
     float tau = sample_tau(rng), m;
@@ -225,7 +228,8 @@ __global__ void k_transmittance_ratio_dda(const DevScene S, BatchParams B) {
     const float len = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
     float dir[3] = {dv[0] / len, dv[1] / len, dv[2] / len};
     float t0, t1;
-    if (len == 0.0f || !aabb_unit<float>(a, dir, 0.0f, len, t0, t1) || !(S.sigma_max_f > 0.0f)) {
+    if (len == 0.0f || !aabb_unit<float>(a, dir, 0.0f, len, t0, t1) || !(S.sigma_max_f > 0.0f) ||
+        !occ_clip(S, a, dir, t0, t1)) {
         B.out[i] = 1.0;
         return;
     }
