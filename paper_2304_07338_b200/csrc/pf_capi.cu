@@ -54,11 +54,15 @@ int set_err(int code, const char *fmt, ...) {
     return code;
 }
 
+// A failed call is reported once: the runtime's (non-sticky) last-error state
+// is cleared so a later, unrelated cudaGetLastError() check does not re-report it.
 #define PF_CUDA(call)                                                                      \
     do {                                                                                   \
         cudaError_t e_ = (call);                                                           \
-        if (e_ != cudaSuccess)                                                             \
+        if (e_ != cudaSuccess) {                                                           \
+            (void)cudaGetLastError();                                                      \
             return set_err(PF_ERR_RUNTIME, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+        }                                                                                  \
     } while (0)
 
 uint64_t splitmix64(uint64_t x) {

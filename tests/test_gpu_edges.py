@@ -125,3 +125,35 @@ def test_async_host_frames_equal_sync(ctx):
         assert np.array_equal(a, b)
     with pytest.raises(ValueError):
         ctx.frame_wait(np.zeros((40, 64, 3), np.float32))
+
+
+def test_async_frames_with_shards_and_errors(ctx):
+    """Async host frames of a shard (other tiles zero) and the API's error paths
+    for the IPC frame and the optimizer state."""
+    import torch
+    from paper_2304_07338_b200 import FieldConfig, RenderConfig
+    from paper_2304_07338_b200 import _lib
+    from paper_2304_07338_b200.scene import CameraSpec, default_lights, synth_volume, tf_scene_b
+    ctx.upload_volume(synth_volume("sphere_sinusoid", 24))
+    ctx.set_medium(tf_scene_b(), 100.0)
+    ctx.set_lights(default_lights())
+    fc = FieldConfig.desk()
+    ctx.load_field(fc, fc.init_params(seed=1, embed_scale=0.2))
+    cam = CameraSpec(48, 32)
+    rc = RenderConfig(spp=2, seed=5, mode="fast", tile=(16, 16), shard_index=1, shard_count=2)
+    buf = torch.full((32, 48, 3), 7.0, dtype=torch.float32).pin_memory()
+    ctx.render_neural_async(cam, rc, buf.numpy())
+    ctx.frame_wait(buf.numpy())
+    dev = torch.zeros((32, 48, 3), dtype=torch.float32, device="cuda")
+    ctx.render_neural(cam, rc, out=dev)
+    ctx.synchronize()
+    assert np.array_equal(buf.numpy(), dev.cpu().numpy())   # untouched shards are zero, not stale
+    # IPC handle of nothing -> runtime error (never a silent fallback)
+    with pytest.raises(RuntimeError):
+        ctx.ipc_frame_open(bytes(64), 32, 48)
+    # optimizer state of the wrong size -> invalid argument
+    ctx.train_init(fc, fc.init_params(seed=1))
+    n, _ = ctx.train_counts()
+    bad = np.zeros(n - 1, np.float32)
+    rc_ = _lib.lib().pf_train_state_set(ctx._h, bad.ctypes.data, bad.ctypes.data, bad.ctypes.data, n - 1)
+    assert rc_ == 1
