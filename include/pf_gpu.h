@@ -319,6 +319,20 @@ int pf_train_step(pf_ctx *ctx, size_t n, const float *x3, const float *w_sph2, c
 int pf_train_grad(pf_ctx *ctx, size_t n, const float *x3, const float *w_sph2, const float *g,
                   const float *targets3, double *loss, float *grad, uint8_t *touched);
 int pf_train_counts(pf_ctx *ctx, size_t *n_params, size_t *n_table_entries);
+/* Data-parallel training (one process per GPU): train_step split
+ * around a gradient all-reduce.  pf_train_backward runs forward, loss and
+ * backward of this rank's shard (n of the n_global queries of the step) into
+ * the context's gradient buffers, scaled so their SUM over ranks is the
+ * global-batch gradient (loss_part likewise sums to the global loss).
+ * pf_train_grad_buffers exposes them for an in-place all-reduce: table
+ * gradients as int64 fixed point (n_tab, SUM -- integer, so exact and
+ * independent of the reduction order), MLP gradients binary32 (n_mlp, SUM),
+ * touched flags uint8 (n_entries, MAX).  pf_train_apply then runs Adam. */
+int pf_train_backward(pf_ctx *ctx, size_t n, const float *x3, const float *w_sph2, const float *g,
+                      const float *targets3, size_t n_global, double *loss_part);
+int pf_train_grad_buffers(pf_ctx *ctx, void **gtab, size_t *n_tab, void **gmlp, size_t *n_mlp,
+                          void **touched, size_t *n_entries);
+int pf_train_apply(pf_ctx *ctx, uint64_t step, uint64_t total_steps);
 /* Master parameters (host or device memory, n = n_params). */
 int pf_train_params(pf_ctx *ctx, float *out, size_t n);
 /* Master parameters -> the inference field used by pf_field_query / renders. */

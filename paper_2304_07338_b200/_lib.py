@@ -146,6 +146,10 @@ _SIG = {
     "pf_ipc_frame_release": (C.c_int, [_P, _P, C.c_int]),
     "pf_render_neural_async": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), _P]),
     "pf_frame_wait": (C.c_int, [_P, _P]),
+    "pf_train_backward": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_size_t, _P]),
+    "pf_train_grad_buffers": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_size_t), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "pf_train_apply": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
 }
 EXPORTS = tuple(_SIG)
 

@@ -409,6 +409,34 @@ class Context:
         check(lib().pf_train_grad(self._h, n, *ptrs, C.byref(loss), grad.ctypes.data, touched.ctypes.data))
         return loss.value, grad, touched
 
+    # ---- data-parallel training: backward -> all-reduce -> apply
+    def train_backward(self, x3, wsph2, g, targets3, n_global: int) -> float:
+        """This rank's shard of a step; returns its part of the global loss."""
+        n, ptrs, keep = self._batch(x3, wsph2, g, targets3)
+        loss = C.c_double()
+        check(lib().pf_train_backward(self._h, n, *ptrs, int(n_global), C.byref(loss)))
+        return loss.value
+
+    def train_grad_tensors(self):
+        """Zero-copy CUDA views of the gradient state: (int64 table gradient in
+        2^-40 fixed point, float32 MLP gradient, uint8 touched flags)."""
+        import torch
+        gt, gm, tc = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        nt, nm, ne = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        check(lib().pf_train_grad_buffers(self._h, C.byref(gt), C.byref(nt), C.byref(gm), C.byref(nm), C.byref(tc),
+                                          C.byref(ne)))
+
+        class _V:
+            def __init__(self, ptr, n, ts):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": ts, "data": (ptr, False), "version": 3}
+
+        return (torch.as_tensor(_V(gt.value, nt.value, "<i8"), device="cuda"),
+                torch.as_tensor(_V(gm.value, nm.value, "<f4"), device="cuda"),
+                torch.as_tensor(_V(tc.value, ne.value, "|u1"), device="cuda"))
+
+    def train_apply(self, step: int, total_steps: int) -> None:
+        check(lib().pf_train_apply(self._h, int(step), int(total_steps)))
+
     def train_params(self) -> np.ndarray:
         n_params, _ = self.train_counts()
         out = np.zeros(n_params, np.float32)

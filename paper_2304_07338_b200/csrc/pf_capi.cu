@@ -1487,6 +1487,52 @@ int pf_train_grad(pf_ctx *c, size_t n, const float *x3, const float *w_sph2, con
     return train_common(c, n, x3, w_sph2, g, targets3, 0, 1, false, loss, grad, touched);
 }
 
+int pf_train_backward(pf_ctx *c, size_t n, const float *x3, const float *w_sph2, const float *g,
+                      const float *targets3, size_t n_global, double *loss_part) {
+    if (!c || (n && (!x3 || !w_sph2 || !g || !targets3))) return set_err(PF_ERR_INVALID, "train_backward: null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "train_backward: call pf_train_init first");
+    if (n == 0 || n_global < n) return set_err(PF_ERR_INVALID, "train_backward: need 0 < n <= n_global");
+    PF_CUDA(cudaSetDevice(c->device));
+    TrainState &S = c->train;
+    const void *dx, *dw, *dg, *dt;
+    PF_CUDA(c->stage_in(0, x3, n * 12, &dx));
+    PF_CUDA(c->stage_in(1, w_sph2, n * 8, &dw));
+    PF_CUDA(c->stage_in(2, g, n * 4, &dg));
+    PF_CUDA(c->stage_in(3, targets3, n * 12, &dt));
+    PF_CUDA(S.loss_dev.ensure(8));
+    PF_CUDA(train_backward(S, n, (const float *)dx, (const float *)dw, (const float *)dg, (const float *)dt, n_global, 0,
+                           c->stream));
+    if (loss_part) {
+        PF_CUDA(cudaMemcpyAsync(loss_part, S.loss_dev.p, 8, cudaMemcpyDeviceToHost, c->stream));
+        PF_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return PF_OK;
+}
+
+int pf_train_grad_buffers(pf_ctx *c, void **gtab, size_t *n_tab, void **gmlp, size_t *n_mlp, void **touched,
+                          size_t *n_entries) {
+    if (!c || !gtab || !n_tab || !gmlp || !n_mlp || !touched || !n_entries)
+        return set_err(PF_ERR_INVALID, "pf_train_grad_buffers: null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train_grad_buffers: call pf_train_init first");
+    TrainState &S = c->train;
+    *gtab = S.gtab.p;
+    *n_tab = S.n_tab;
+    *gmlp = S.gmlp.p;
+    *n_mlp = S.n_params - S.n_tab;
+    *touched = S.touched.p;
+    *n_entries = S.n_entries;
+    return PF_OK;
+}
+
+int pf_train_apply(pf_ctx *c, uint64_t step, uint64_t total_steps) {
+    if (!c) return set_err(PF_ERR_INVALID, "null argument");
+    if (!c->train.ready) return set_err(PF_ERR_INVALID, "pf_train_apply: call pf_train_init first");
+    if (total_steps == 0 || step >= total_steps) return set_err(PF_ERR_INVALID, "train_step: need 0 <= step < total");
+    PF_CUDA(cudaSetDevice(c->device));
+    PF_CUDA(train_finish(c->train, step, total_steps, true, nullptr, nullptr, c->stream));
+    return PF_OK;
+}
+
 int pf_train_counts(pf_ctx *c, size_t *n_params, size_t *n_entries) {
     if (!c || !n_params || !n_entries) return set_err(PF_ERR_INVALID, "null argument");
     if (!c->train.ready) return set_err(PF_ERR_INVALID, "call pf_train_init first");

@@ -510,11 +510,10 @@ cudaError_t train_prep(const double *w3, const uint8_t *gidx, const double *t3d,
     return cudaGetLastError();
 }
 
-cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2, const float *g, const float *t3,
-                       uint64_t step, uint64_t total, bool do_update, float *grad_out, uint8_t *touched_out,
-                       size_t loss_slot, int sms, cudaStream_t st) {
-    (void)sms;
+cudaError_t train_backward(TrainState &S, size_t n, const float *x3, const float *w2, const float *g, const float *t3,
+                           size_t n_global, size_t loss_slot, cudaStream_t st) {
     cudaError_t e;
+    if (n_global < n || n_global == 0) n_global = n ? n : 1;
     const size_t ld = (n + 3) & ~(size_t)3;
     const size_t rows = (size_t)S.din + (size_t)S.H * 64 + (size_t)(S.H + 1) * 64;
     if ((e = S.act.ensure(rows * ld * 4))) return e;
@@ -547,7 +546,7 @@ cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2
     T.qg = g;
     T.qt = t3;
     T.eps_rel = (float)S.eps_rel;
-    T.inv_3n = (float)(1.0 / (3.0 * (double)n));
+    T.inv_3n = (float)(1.0 / (3.0 * (double)n_global));  // this shard's part of the global mean
     float *act = (float *)S.act.p;
     T.A0 = act;
     T.A = act + (size_t)S.din * ld;
@@ -566,7 +565,7 @@ cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2
     if (n) {
         if ((e = launch_fb_dispatch(S.Fp, S.Fd, T, (const float4 *)S.img.p, n4, smem, true, st))) return e;
     }
-    k_train_loss<<<1, 1024, 0, st>>>(T.loss_q, n, 1.0 / (3.0 * (double)(n ? n : 1)), (double *)S.loss_dev.p + loss_slot);
+    k_train_loss<<<1, 1024, 0, st>>>(T.loss_q, n, 1.0 / (3.0 * (double)n_global), (double *)S.loss_dev.p + loss_slot);
     if (n) {
         if ((e = launch_fb_dispatch(S.Fp, S.Fd, T, (const float4 *)S.img.p, n4, smem, false, st))) return e;
     }
@@ -586,6 +585,13 @@ cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2
                                                         gmlp + (S.off_w[L] - S.n_tab));
         if ((e = cudaGetLastError())) return e;
     }
+    return cudaSuccess;
+}
+
+cudaError_t train_finish(TrainState &S, uint64_t step, uint64_t total, bool do_update, float *grad_out,
+                         uint8_t *touched_out, cudaStream_t st) {
+    cudaError_t e;
+    float *gmlp = (float *)S.gmlp.p;
     AdamArgs A;
     A.n_params = S.n_params;
     A.n_tab = S.n_tab;
@@ -614,6 +620,15 @@ cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2
     }
     if ((e = cudaGetLastError())) return e;
     return cudaMemsetAsync(S.touched.p, 0, S.n_entries, st);
+}
+
+cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2, const float *g, const float *t3,
+                       uint64_t step, uint64_t total, bool do_update, float *grad_out, uint8_t *touched_out,
+                       size_t loss_slot, int sms, cudaStream_t st) {
+    (void)sms;
+    cudaError_t e = train_backward(S, n, x3, w2, g, t3, n, loss_slot, st);
+    if (e != cudaSuccess) return e;
+    return train_finish(S, step, total, do_update, grad_out, touched_out, st);
 }
 
 }  // namespace pfk

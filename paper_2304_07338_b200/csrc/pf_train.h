@@ -67,6 +67,14 @@ cudaError_t train_init(TrainState &S, const FieldDesc &fd, const std::vector<Fie
 cudaError_t train_step(TrainState &S, size_t n, const float *x3, const float *w2, const float *g, const float *t3,
                        uint64_t step, uint64_t total, bool do_update, float *grad_out, uint8_t *touched_out,
                        size_t loss_slot, int sms, cudaStream_t st);
+// The two halves of train_step for data-parallel training: backward scales
+// the loss / gradient by 1 / (3 n_global) so that summing the gradient
+// buffers over ranks gives the global batch mean; finish applies Adam (or
+// exports the gradient) and clears the accumulators.
+cudaError_t train_backward(TrainState &S, size_t n, const float *x3, const float *w2, const float *g, const float *t3,
+                           size_t n_global, size_t loss_slot, cudaStream_t st);
+cudaError_t train_finish(TrainState &S, uint64_t step, uint64_t total, bool do_update, float *grad_out,
+                         uint8_t *touched_out, cudaStream_t st);
 // make_batch outputs (binary64 directions / targets, phase indices) -> the
 // trainer's binary32 inputs: w_sph = (theta/pi, (phi+pi)/2pi), g = phase[gidx].
 cudaError_t train_prep(const double *w3, const uint8_t *gidx, const double *t3d, const double *phase, int n_phases,

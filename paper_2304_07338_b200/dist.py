@@ -122,6 +122,31 @@ def render_frame_p2p(ctx, cam, rc, shared_frame, sync, group=None):
     return shared_frame
 
 
+def train_step_dp(ctx, x3, wsph2, g, targets3, n_global: int, step: int, total: int, group=None) -> float:
+    """Data-parallel train_step (one process per GPU): this rank's shard
+    backward, all-reduce of the gradient state (int64 fixed-point table sums --
+    exact and order-independent -- float32 MLP sums, touched flags by MAX),
+    then Adam on every rank with identical inputs.  Returns the global loss."""
+    import torch
+    import torch.distributed as dist
+    loss = ctx.train_backward(x3, wsph2, g, targets3, n_global)
+    gtab, gmlp, touched = ctx.train_grad_tensors()
+    ctx.synchronize()
+    host = dist.get_backend(group) != "nccl"  # gloo: reduce host copies
+    for buf, op in ((gtab, dist.ReduceOp.SUM), (gmlp, dist.ReduceOp.SUM), (touched, dist.ReduceOp.MAX)):
+        t = buf.to(torch.int32) if buf.dtype == torch.uint8 else buf
+        if host:
+            t = t.cpu()
+        dist.all_reduce(t, op=op, group=group)
+        buf.copy_(t.to(buf.dtype))
+    lt = torch.tensor([loss], dtype=torch.float64)
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=group)
+    if gtab.is_cuda:
+        torch.cuda.synchronize()
+    ctx.train_apply(step, total)
+    return float(lt.item())
+
+
 def _check_cover(width, height, tile_w, tile_h, count) -> bool:
     seen = np.zeros((height, width), np.int32)
     for s in range(count):

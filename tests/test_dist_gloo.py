@@ -75,3 +75,79 @@ def test_tile_cover_properties():
         assert _check_cover(W, H, TW, TH, count)
         sizes = [len(shard_tiles(1920, 1080, 16, 16, s, count)) for s in range(count)]
         assert max(sizes) * 16 * 16 * 3 == packed_floats(1920, 1080, 16, 16, count)
+
+
+class _ShardCtx:
+    """Stands in for Context in train_step_dp on CPU: the oracle computes this
+    rank's shard gradient (scaled to its part of the global mean), stored the
+    way the device keeps it (int64 2^-40 fixed-point tables, float32 MLP,
+    uint8 touched flags)."""
+
+    def __init__(self, fc, params):
+        sys.path.insert(0, str(ROOT))
+        from oracle import oracle as o
+        self.o, self.fc, self.params = o, fc, params
+        self.n_tab = len(params) - o._mlp_count(fc)
+
+    def train_backward(self, x, w, g, t, n_global):
+        import torch
+        loss, grad, touched = self.o.train_grad(self.fc, self.params, x, w, g, t)
+        s = len(x) / n_global
+        self.gtab = torch.from_numpy(np.rint(grad[:self.n_tab] * s * 2.0 ** 40).astype(np.int64))
+        self.gmlp = torch.from_numpy((grad[self.n_tab:] * s).astype(np.float32))
+        self.touched = torch.from_numpy(touched.astype(np.uint8))
+        return loss * s
+
+    def train_grad_tensors(self):
+        return self.gtab, self.gmlp, self.touched
+
+    def synchronize(self):
+        pass
+
+    def train_apply(self, step, total):
+        self.applied = (step, total)
+
+
+def _dp_batch():
+    r = np.random.default_rng(3)
+    n = 48
+    return [r.random((n, 3)), r.random((n, 2)), r.choice([-0.75, 0.0, 0.75], n), r.random((n, 3))]
+
+
+def _dp_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2304_07338_b200 import FieldConfig
+    from paper_2304_07338_b200.dist import train_step_dp
+    fc = FieldConfig.desk()
+    ctx = _ShardCtx(fc, fc.init_params(seed=4, embed_scale=0.1, bias_scale=0.05).astype(np.float64))
+    b = _dp_batch()
+    n = len(b[0])
+    lo, hi = rank * n // world, (rank + 1) * n // world
+    loss = train_step_dp(ctx, *(a[lo:hi] for a in b), n_global=n, step=2, total=10)
+    assert ctx.applied == (2, 10)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), loss=loss, gtab=ctx.gtab.numpy(), gmlp=ctx.gmlp.numpy(),
+             touched=ctx.touched.numpy())
+    dist.destroy_process_group()
+
+
+def test_data_parallel_gradient_reduction(tmp_path):
+    """dist.train_step_dp: SUM of the fixed-point table and MLP gradients, MAX
+    of the touched flags, SUM of the loss parts == the full-batch step."""
+    mp.spawn(_dp_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle as o
+    from paper_2304_07338_b200 import FieldConfig
+    fc = FieldConfig.desk()
+    params = fc.init_params(seed=4, embed_scale=0.1, bias_scale=0.05).astype(np.float64)
+    loss, grad, touched = o.train_grad(fc, params, *_dp_batch())
+    n_tab = len(params) - o._mlp_count(fc)
+    r0, r1 = np.load(tmp_path / "r0.npz"), np.load(tmp_path / "r1.npz")
+    for k in ("gtab", "gmlp", "touched", "loss"):
+        assert np.array_equal(r0[k], r1[k]), k
+    assert abs(float(r0["loss"]) - loss) <= 1e-12 * loss
+    assert np.array_equal(r0["touched"], touched.astype(np.uint8))
+    assert np.max(np.abs(r0["gtab"] / 2.0 ** 40 - grad[:n_tab])) <= 4e-12
+    assert np.allclose(r0["gmlp"], grad[n_tab:], rtol=1e-5, atol=1e-7 * np.abs(grad[n_tab:]).max())
