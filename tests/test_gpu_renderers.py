@@ -219,3 +219,41 @@ def test_two_lights_three_trials_parity(ctx, oracle):
     got = ctx.render_neural(cam, rc2)
     ref, _ = oracle.render_neural(osc, lights, None, None, cam, rc2)
     assert _rel_mismatch(got, ref, 1e-12) <= 3
+
+
+def test_path_traced_noise_falls_with_spp(ctx):
+    """pixel variance at 1 spp > at 64 spp (same scene, same pixels)."""
+    ctx.upload_volume(synth_volume("sphere_sinusoid", 32))
+    ctx.set_medium(tf_scene_b(), 100.0)
+    ctx.set_lights(default_lights())
+    cam = CameraSpec(32, 32)
+    pt = PathTraceConfig(max_bounces=8)
+
+    def var(spp):
+        a, b = (ctx.render_path_traced(cam, RenderConfig(spp=spp, g=0.3, seed=s, mode="fast"), pt).astype(np.float64)
+                for s in (1, 2))
+        return np.mean((a - b) ** 2) / 2
+    v1, v64 = var(1), var(64)
+    print("pt pixel variance 1 spp", v1, "64 spp", v64)
+    assert v1 > 8 * v64
+
+
+def test_photon_map_consistency_with_photon_count(ctx):
+    """more photons -> strictly lower MSE against a dense-map
+    reference render (median over 3 seeds), with maps traced on the device."""
+    from paper_2304_07338_b200 import TraceConfig
+    ctx.upload_volume(synth_volume("sphere_sinusoid", 32))
+    ctx.set_medium(tf_scene_b(), 100.0)
+    ctx.set_lights(default_lights())
+    cam = CameraSpec(48, 48)
+    rc = RenderConfig(spp=16, g=0.0, seed=3, mode="fast", w_d=0.0)
+
+    def render(n, seed):
+        tc = TraceConfig(n_total=n, seed=seed)
+        ctx.trace_photons(tc, device=True)
+        ctx.knn_build_traced(tc.phase_set)
+        return ctx.render_photon_map(cam, rc, K=64).astype(np.float64)
+    ref = render(8_000_000, 99)
+    med = [np.median([np.mean((render(n, s) - ref) ** 2) for s in range(3)]) for n in (10_000, 100_000, 1_000_000)]
+    print("pm mse vs photon count", med)
+    assert med[0] > med[1] > med[2]
