@@ -68,9 +68,15 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
     const int lane = threadIdx.x & 31;
     const size_t warp0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const size_t n_warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    const size_t n_rg = n_rows >> 3;
     for (size_t wu = warp0; wu < n_wu; wu += n_warps) {
-        const size_t row = (wu / U4) * 8 + (lane & 7);
-        const int u = (int)(wu % U4) * 4 + (lane >> 3);
+        // level-major: the whole grid sweeps all rows for one group of 4
+        // levels before the next, so the tables in use (4 x <= 8 MB at the
+        // paper config) stay L2-resident instead of being gathered from DRAM
+        const size_t rg = P.level_major ? wu % n_rg : wu / U4;
+        const int ug = P.level_major ? (int)(wu / n_rg) : (int)(wu % U4);
+        const size_t row = rg * 8 + (lane & 7);
+        const int u = ug * 4 + (lane >> 3);
         if (u >= U) continue;
         const bool valid = row < n;
         const size_t gr = P.row0 + row;  // global item index
@@ -445,7 +451,13 @@ size_t field_feat_bytes(const FieldHost &h, size_t n_items) {
 }
 
 template <int FP, int FD>
-static cudaError_t launch_encode(const FieldParams &P, int grid, cudaStream_t st) {
+static cudaError_t launch_encode(const FieldParams &P0, int grid, cudaStream_t st) {
+    static const int order = [] {
+        const char *e = std::getenv("PF_ENCODE_ORDER");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    FieldParams P = P0;
+    P.level_major = order;
     k_field_encode<FP, FD><<<grid, 256, 0, st>>>(P);
     return cudaGetLastError();
 }
