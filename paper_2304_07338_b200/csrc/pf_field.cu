@@ -64,18 +64,21 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
     const size_t n = n_all > P.row0 ? min(n_all - P.row0, P.row_cap) : 0;  // rows of this launch
     const size_t n_rows = (n + 127) & ~(size_t)127;  // whole tiles (pad rows encode zeros)
     const int U = P.n_pos_levels + P.n_dir_levels + 1, U4 = (U + 3) >> 2;
-    const size_t n_wu = (n_rows >> 3) * (size_t)U4;
     const int lane = threadIdx.x & 31;
-    const size_t warp0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const size_t n_warps = ((size_t)gridDim.x * blockDim.x) >> 5;
-    const size_t n_rg = n_rows >> 3;
-    for (size_t wu = warp0; wu < n_wu; wu += n_warps) {
-        // level-major: the whole grid sweeps all rows for one group of 4
-        // levels before the next, so the tables in use (4 x <= 8 MB at the
-        // paper config) stay L2-resident instead of being gathered from DRAM
-        const size_t rg = P.level_major ? wu % n_rg : wu / U4;
-        const int ug = P.level_major ? (int)(wu / n_rg) : (int)(wu % U4);
-        const size_t row = rg * 8 + (lane & 7);
+    const uint32_t warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_rg = (uint32_t)(n_rows >> 3);  // 8-row groups (< 2^29: render rows < 2^32)
+    // per-level addressing in shared memory: each warp reads 4 different
+    // levels, which a dynamically indexed kernel-parameter load serialises
+    __shared__ FieldLevel s_lv[PF_FIELD_MAX_LEVELS];
+    for (int i = threadIdx.x; i < U - 1 && i < PF_FIELD_MAX_LEVELS; i += blockDim.x) s_lv[i] = P.lv[i];
+    __syncthreads();
+    // level-major: the whole grid sweeps all rows for one group of 4 levels
+    // before the next, so the tables in use (4 x <= 8 MB at the paper config)
+    // stay L2-resident instead of being gathered from DRAM
+    for (int ug = 0; ug < U4; ++ug)
+    for (uint32_t rg = warp0; rg < n_rg; rg += n_warps) {
+        const size_t row = (size_t)rg * 8 + (lane & 7);
         const int u = ug * 4 + (lane >> 3);
         if (u >= U) continue;
         const bool valid = row < n;
@@ -96,13 +99,13 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
         if (u < P.n_pos_levels) {
             float pin[3] = {__saturatef(x[0]), __saturatef(x[1]), __saturatef(x[2])};
             float acc[FP];
-            encode_level<3, FP>(P, u, pin, acc);
+            encode_level<3, FP>(P.tables, s_lv[u], pin, acc);
             st_feats_global<FP>(P.feat + feat_off(P, row, u * FP), acc);
         } else if (u < P.n_pos_levels + P.n_dir_levels) {
             const int l = u - P.n_pos_levels;
             float pin[2] = {__saturatef(ws[0]), __saturatef(ws[1])};
             float acc[FD];
-            encode_level<2, FD>(P, P.n_pos_levels + l, pin, acc);
+            encode_level<2, FD>(P.tables, s_lv[P.n_pos_levels + l], pin, acc);
             st_feats_global<FD>(P.feat + feat_off(P, row, P.n_pos_levels * FP + l * FD), acc);
         } else {
             const int kg = P.n_pos_levels * FP + P.n_dir_levels * FD;  // multiple of 8
@@ -452,12 +455,7 @@ size_t field_feat_bytes(const FieldHost &h, size_t n_items) {
 
 template <int FP, int FD>
 static cudaError_t launch_encode(const FieldParams &P0, int grid, cudaStream_t st) {
-    static const int order = [] {
-        const char *e = std::getenv("PF_ENCODE_ORDER");
-        return e && e[0] == '0' ? 0 : 1;
-    }();
-    FieldParams P = P0;
-    P.level_major = order;
+    const FieldParams &P = P0;
     k_field_encode<FP, FD><<<grid, 256, 0, st>>>(P);
     return cudaGetLastError();
 }

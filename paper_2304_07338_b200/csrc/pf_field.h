@@ -59,7 +59,6 @@ struct FieldParams {
     uint8_t *feat;     // [tile][chunk][16 KB], UMMA canonical K-major fp16
     int nch;           // 64-column chunks per tile (last one may be narrower)
     size_t row0, row_cap;  // this launch handles items [row0, row0 + row_cap)
-    int level_major;       // encode work order (set by launch_field)
 };
 
 struct FieldHost {

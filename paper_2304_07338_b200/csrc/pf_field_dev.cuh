@@ -83,19 +83,23 @@ __device__ __forceinline__ void issue_layer(uint32_t a_s, uint32_t b_s, int K, i
 // Encode ONE level of one input (pinned in oracle
 // or_hashgrid_encode): 2^D gathers issued back to back, fp32 accumulation.
 template <int D, int F>
-__device__ __forceinline__ void encode_level(const FieldParams &P, int lv, const float *pin, float *acc) {
+__device__ __forceinline__ void encode_level(const __half *tables, const FieldLevel L, const float *pin, float *acc) {
     constexpr int NC = 1 << D;
-    const FieldLevel L = P.lv[lv];
     uint32_t c[D];
     float f[D];
     level_cell<D>(L, pin, c, f);
     Raw<F> e[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) e[k] = load_raw<F>(P.tables + L.offset_halves, corner_index<D>(L, c, k));
+    for (int k = 0; k < NC; ++k) e[k] = load_raw<F>(tables + L.offset_halves, corner_index<D>(L, c, k));
 #pragma unroll
     for (int k = 0; k < F; ++k) acc[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) accum_raw<F>(e[k], corner_weight<D>(f, k), acc);
+}
+
+template <int D, int F>
+__device__ __forceinline__ void encode_level(const FieldParams &P, int lv, const float *pin, float *acc) {
+    encode_level<D, F>(P.tables, P.lv[lv], pin, acc);
 }
 
 }  // namespace pfk
