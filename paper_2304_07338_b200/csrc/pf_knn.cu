@@ -1137,7 +1137,12 @@ cudaError_t knn_query(const KnnParams &P, cudaStream_t st) {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const unsigned blocks = (unsigned)std::min<size_t>(P.nq, (size_t)sms * 3);
+        static const int per_sm = [] {
+            const char *e = std::getenv("PF_KNN_CTA_PER_SM");
+            const int v = e ? std::atoi(e) : 3;
+            return v >= 1 && v <= 4 ? v : 3;
+        }();
+        const unsigned blocks = (unsigned)std::min<size_t>(P.nq, (size_t)sms * per_sm);
         k_knn_query_cta<<<blocks, kCtaThreads, 0, st>>>(P);
         return cudaGetLastError();
     }
