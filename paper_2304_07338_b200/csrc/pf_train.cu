@@ -15,9 +15,12 @@
 //                  kept feature-major [k][query] (coalesced across the warp)
 //                  for the backward pass; loss term + dloss/dz_H;
 //   k_train_bwd    one thread per query: dz_{L-1} = (W_L^T dz_L) . [a_L > 0],
-//                  then dfeat = W_0^T dz_0 scattered into the tables with
-//                  fixed-point integer atomics (deterministic: integer adds
-//                  are associative) + touched flags (sparse Adam);
+//                  then dfeat = W_0^T dz_0 (feature-major rows);
+//   k_train_scatter one thread per (query, level), level-major grid (the
+//                  level's gradient slab stays L2-resident): dfeat scattered
+//                  into the tables with fixed-point integer atomics
+//                  (deterministic: integer adds are associative) + touched
+//                  flags (sparse Adam);
 //   k_train_wgrad  dW_L = dZ_L . In_L^T (+ db_L via a virtual ones row) as
 //                  a tiled SIMT GEMM over query chunks -> per-chunk partials;
 //   k_train_wsum   partials summed in chunk order (deterministic);
@@ -198,12 +201,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_fwd(const TrainParams T, 
 }
 
 template <int D, int F>
-__device__ __forceinline__ void level_scatter(const TrainParams &T, int lv, const float *pin, const float *W0, int k0,
-                                              const float *dz, uint32_t entry_base, uint32_t tab_base, int Fdiv) {
+__device__ __forceinline__ void level_scatter(const TrainParams &T, int lv, const float *pin, int k0, size_t q,
+                                              uint32_t entry_base, uint32_t tab_base, int Fdiv) {
     const FieldLevel L = T.lv[lv];
     float dfeat[F];
 #pragma unroll
-    for (int k = 0; k < F; ++k) dfeat[k] = dot64(W0 + (k0 + k) * 64, dz);
+    for (int k = 0; k < F; ++k) dfeat[k] = T.dF[(size_t)(k0 + k) * T.ld + q];
     uint32_t c[D];
     float f[D];
     level_cell<D>(L, pin, c, f);
@@ -215,6 +218,24 @@ __device__ __forceinline__ void level_scatter(const TrainParams &T, int lv, cons
 #pragma unroll
         for (int k = 0; k < F; ++k) fix_add(gp + k, w * dfeat[k]);
         T.touched[entry_base + (L.offset_halves - tab_base) / (uint32_t)Fdiv + idx] = 1;
+    }
+}
+
+// grid (query blocks, levels): blockIdx.y is the level, so the CTAs of one
+// level run together and its fixed-point gradient slab stays in L2
+template <int FP, int FD>
+__global__ void __launch_bounds__(256) k_train_scatter(const TrainParams T) {
+    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= T.n) return;
+    const int lv = blockIdx.y;
+    if (lv < T.n_pos_levels) {
+        const float pin[3] = {__saturatef(T.qx[3 * q]), __saturatef(T.qx[3 * q + 1]), __saturatef(T.qx[3 * q + 2])};
+        level_scatter<3, FP>(T, lv, pin, lv * FP, q, 0u, 0u, FP);
+    } else {
+        const int l = lv - T.n_pos_levels;
+        const float pin[2] = {__saturatef(T.qw[2 * q]), __saturatef(T.qw[2 * q + 1])};
+        level_scatter<2, FD>(T, lv, pin, T.n_pos_levels * FP + l * FD, q, T.n_pos_tab / (uint32_t)FP, T.n_pos_tab,
+                             FD);
     }
 }
 
@@ -256,20 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_bwd(const TrainParams T, 
 #pragma unroll
         for (int k = 0; k < 64; ++k) dz[k] = out[(size_t)k * ld + q];
     }
-    // ---- dfeat = W_0^T dz_0 -> tables (row j of W_0^T is W_0[:, j])
-    // W_0^T is stored [k][o], so (W_0^T dz)_k = sum_o W0T[k][o] dz_o
+    // ---- dfeat = W_0^T dz_0 (row j of W_0^T is W_0[:, j]) -> feature-major
+    // rows for k_train_scatter.  W_0^T is stored [k][o], so
+    // (W_0^T dz)_k = sum_o W0T[k][o] dz_o
     const float *W0 = sm + T.wt_off[0];
-    {
-        const float pin[3] = {__saturatef(T.qx[3 * q]), __saturatef(T.qx[3 * q + 1]), __saturatef(T.qx[3 * q + 2])};
-        for (int l = 0; l < T.n_pos_levels; ++l) level_scatter<3, FP>(T, l, pin, W0, l * FP, dz, 0u, 0u, FP);
-    }
-    {
-        const float pin[2] = {__saturatef(T.qw[2 * q]), __saturatef(T.qw[2 * q + 1])};
-        const int k0 = T.n_pos_levels * FP;
-        const uint32_t ebase = T.n_pos_tab / (uint32_t)FP;
-        for (int l = 0; l < T.n_dir_levels; ++l)
-            level_scatter<2, FD>(T, T.n_pos_levels + l, pin, W0, k0 + l * FD, dz, ebase, T.n_pos_tab, FD);
-    }
+    const int n_tab_feats = T.n_pos_levels * FP + T.n_dir_levels * FD;
+#pragma unroll 2
+    for (int k = 0; k < n_tab_feats; ++k) T.dF[(size_t)k * ld + q] = dot64(W0 + k * 64, dz);
 }
 
 // dW_L partials: part[chunk][o][k] = sum_{q in chunk} dZ_L[o][q] In_L[k][q],
@@ -442,6 +456,10 @@ cudaError_t launch_fb(const TrainParams &T, const float4 *img, int n4, size_t sm
     } else {
         cudaFuncSetAttribute(k_train_bwd<FP, FD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_train_bwd<FP, FD><<<blocks, kThreads, smem, st>>>(T, img, n4);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const dim3 sg((unsigned)((T.n + 255) / 256), (unsigned)(T.n_pos_levels + T.n_dir_levels));
+        k_train_scatter<FP, FD><<<sg, 256, 0, st>>>(T);
     }
     return cudaGetLastError();
 }
@@ -515,7 +533,7 @@ cudaError_t train_backward(TrainState &S, size_t n, const float *x3, const float
     cudaError_t e;
     if (n_global < n || n_global == 0) n_global = n ? n : 1;
     const size_t ld = (n + 3) & ~(size_t)3;
-    const size_t rows = (size_t)S.din + (size_t)S.H * 64 + (size_t)(S.H + 1) * 64;
+    const size_t rows = 2 * (size_t)S.din + (size_t)S.H * 64 + (size_t)(S.H + 1) * 64;
     if ((e = S.act.ensure(rows * ld * 4))) return e;
     if ((e = S.lossq.ensure(n * 4 + 16))) return e;
     if ((e = S.loss_dev.ensure((loss_slot + 1) * 8))) return e;
@@ -551,6 +569,7 @@ cudaError_t train_backward(TrainState &S, size_t n, const float *x3, const float
     T.A0 = act;
     T.A = act + (size_t)S.din * ld;
     T.dZ = T.A + (size_t)S.H * 64 * ld;
+    T.dF = T.dZ + (size_t)(S.H + 1) * 64 * ld;
     T.loss_q = (float *)S.lossq.p;
     T.gtab = (unsigned long long *)S.gtab.p;
     T.touched = (uint8_t *)S.touched.p;

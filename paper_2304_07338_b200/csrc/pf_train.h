@@ -30,6 +30,7 @@ struct TrainParams {
     float *A;                            // H x 64 rows: a_1 .. a_H (post-ReLU)
     float *dZ;                           // (H + 1) x 64 rows: dloss/dz_0 .. dz_H
     float *loss_q;                       // per-query sum over channels of (p-t)^2/(p^2+eps)
+    float *dF;                           // table-feature rows [k][ld]: dloss/dfeature (k_train_bwd -> k_train_scatter)
     unsigned long long *gtab;            // fixed-point table gradient (n_tab)
     uint8_t *touched;                    // per table entry (pos entries, then dir)
 };
