@@ -147,6 +147,91 @@ def train_step_dp(ctx, x3, wsph2, g, targets3, n_global: int, step: int, total: 
     return float(lt.item())
 
 
+def _bcast_array(a, src, group, device):
+    """Broadcast a numpy array from rank src (shape/dtype travel as an object);
+    returns a torch tensor on `device` on every rank."""
+    import torch
+    import torch.distributed as dist
+    meta = [None if a is None else (tuple(a.shape), str(a.dtype))]
+    dist.broadcast_object_list(meta, src=src, group=group)
+    if meta[0] is None:
+        return None
+    shape, dt = meta[0]
+    if dist.get_rank(group) == src:
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    else:
+        t = torch.empty(shape, dtype=getattr(torch, np.dtype(dt).name), device=device)
+    dist.broadcast(t, src=src, group=group)
+    return t
+
+
+def broadcast_scene(ctx, volume=None, tf_points=None, density_scale: float = 100.0, lights=None,
+                    field=None, photons=None, phase_set=None, src: int = 0, group=None) -> None:
+    """Replicate the scene on every rank (volume, TF, lights
+    and field weights are broadcast from rank `src` on a scene / TF change and
+    uploaded into each rank's context; the photon map likewise, rebuilt into
+    each rank's KNN index).  Arguments are only read on `src`; `field` is
+    (FieldConfig, params), `photons` a PHOTON_DTYPE array with its phase set.  Large arrays travel as device tensors
+    over NCCL (host tensors over gloo); the small TF / light / config records
+    as pickled objects."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    small = [None]
+    if dist.get_rank(group) == src:
+        small[0] = (None if tf_points is None else np.asarray(tf_points, np.float64), float(density_scale),
+                    None if lights is None else np.asarray(lights, np.float64),
+                    None if field is None else field[0], None if phase_set is None else list(phase_set))
+    dist.broadcast_object_list(small, src=src, group=group)
+    tf, ds, li, fc, ps = small[0]
+    vol = _bcast_array(None if volume is None else np.asarray(volume, np.float32), src, group, dev)
+    par = _bcast_array(None if field is None else np.asarray(field[1], np.float32), src, group, dev)
+    phb = _bcast_array(None if photons is None else np.ascontiguousarray(photons).view(np.uint8), src, group, dev)
+    if vol is not None:
+        ctx.upload_volume(vol)
+    if tf is not None:
+        ctx.set_medium(tf, ds)
+    if li is not None:
+        ctx.set_lights(li)
+    if fc is not None:
+        ctx.load_field(fc, par)
+    if phb is not None:
+        from .scene import PHOTON_DTYPE
+        ctx.knn_build(phb.cpu().numpy().view(PHOTON_DTYPE), ps)
+    if dev == "cuda":
+        torch.cuda.synchronize()
+
+
+def shard_rows(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced row range [lo, hi) of rank `rank`."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+def knn_targets_sharded(ctx, x3, w3, gidx, K: int, r_max: float = float("inf"), psi: float = 5.0,
+                        group=None) -> np.ndarray:
+    """Training targets of a query batch split over ranks (SURVEY.md 8(e),
+    KNN C3): each rank runs the KNN gather + Eq. 6/7 on its contiguous share
+    of the queries against its replica of the photon map, then one all_gather
+    assembles the (n, 3) binary64 targets on every rank.  Queries are
+    independent, so the result is byte-identical to a single-GPU call."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = int(np.asarray(x3).shape[0])
+    lo, hi = shard_rows(n, rank, world)
+    part = ctx.knn_targets(np.asarray(x3)[lo:hi], np.asarray(w3)[lo:hi], np.asarray(gidx)[lo:hi], K, r_max, psi)
+    per = -(-n // world)  # padded share
+    buf = np.zeros((per, 3), np.float64)
+    buf[:hi - lo] = part
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.from_numpy(buf).to(dev)
+    out = torch.empty((world * per, 3), dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(out, t, group=group)
+    out = out.cpu().numpy()
+    return np.concatenate([out[r * per:r * per + (shard_rows(n, r, world)[1] - shard_rows(n, r, world)[0])]
+                           for r in range(world)])
+
+
 def _check_cover(width, height, tile_w, tile_h, count) -> bool:
     seen = np.zeros((height, width), np.int32)
     for s in range(count):

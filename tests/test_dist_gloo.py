@@ -151,3 +151,68 @@ def test_data_parallel_gradient_reduction(tmp_path):
     assert np.array_equal(r0["touched"], touched.astype(np.uint8))
     assert np.max(np.abs(r0["gtab"] / 2.0 ** 40 - grad[:n_tab])) <= 4e-12
     assert np.allclose(r0["gmlp"], grad[n_tab:], rtol=1e-5, atol=1e-7 * np.abs(grad[n_tab:]).max())
+
+
+class _RecCtx:
+    """Records what broadcast_scene uploads; knn_targets is a per-row function."""
+
+    def __init__(self):
+        self.got = {}
+
+    def upload_volume(self, v):
+        self.got["volume"] = np.asarray(v).copy()
+
+    def set_medium(self, tf, ds):
+        self.got["tf"], self.got["ds"] = np.asarray(tf).copy(), ds
+
+    def set_lights(self, li):
+        self.got["lights"] = np.asarray(li).copy()
+
+    def load_field(self, fc, params):
+        self.got["fc"], self.got["params"] = fc, np.asarray(params).copy()
+
+    def knn_targets(self, x3, w3, gidx, K, r_max, psi):
+        return np.asarray(x3, np.float64) * 2.0 + np.asarray(w3) * K + np.asarray(gidx)[:, None] / psi
+
+
+def _scene_arrays():
+    from paper_2304_07338_b200 import FieldConfig
+    from paper_2304_07338_b200.scene import default_lights, synth_volume, tf_scene_b
+    fc = FieldConfig.desk()
+    return synth_volume("sphere_sinusoid", 12), tf_scene_b(), default_lights(), fc, fc.init_params(seed=3)
+
+
+def _bq_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2304_07338_b200.dist import broadcast_scene, knn_targets_sharded
+    ctx = _RecCtx()
+    if rank == 0:
+        vol, tf, li, fc, par = _scene_arrays()
+        broadcast_scene(ctx, vol, tf, 50.0, li, (fc, par))
+    else:
+        broadcast_scene(ctx)
+    r = np.random.default_rng(1)
+    n = 37  # not a multiple of the world size
+    x, w, g = r.random((n, 3)).astype(np.float32), r.random((n, 3)), r.integers(0, 3, n).astype(np.uint8)
+    t = knn_targets_sharded(ctx, x, w, g, K=8, r_max=0.5, psi=5.0)
+    np.savez(os.path.join(out_dir, f"s{rank}.npz"), t=t, ds=ctx.got["ds"],
+             **{k: ctx.got[k] for k in ("volume", "tf", "lights", "params")})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_scene_broadcast_and_sharded_targets(tmp_path, world):
+    mp.spawn(_bq_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    vol, tf, li, fc, par = _scene_arrays()
+    r = np.random.default_rng(1)
+    n = 37
+    x, w, g = r.random((n, 3)).astype(np.float32), r.random((n, 3)), r.integers(0, 3, n).astype(np.uint8)
+    ref = _RecCtx().knn_targets(x, w, g, 8, 0.5, 5.0)
+    for k in range(world):
+        d = np.load(tmp_path / f"s{k}.npz")
+        assert np.array_equal(d["volume"], vol) and np.array_equal(d["tf"], tf)
+        assert np.array_equal(d["lights"], li) and np.array_equal(d["params"], par) and float(d["ds"]) == 50.0
+        assert np.array_equal(d["t"], ref)
