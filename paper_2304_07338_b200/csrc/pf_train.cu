@@ -361,6 +361,33 @@ struct AdamArgs {
     const uint8_t *touched;
 };
 
+template <int F>
+__device__ __forceinline__ void ld_vec(const float *a, float (&r)[F]) {
+    if constexpr (F % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < F; k += 4) {
+            const float4 x = *reinterpret_cast<const float4 *>(a + k);
+            r[k] = x.x, r[k + 1] = x.y, r[k + 2] = x.z, r[k + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < F; k += 2) {
+            const float2 x = *reinterpret_cast<const float2 *>(a + k);
+            r[k] = x.x, r[k + 1] = x.y;
+        }
+    }
+}
+template <int F>
+__device__ __forceinline__ void st_vec(float *a, const float (&r)[F]) {
+    if constexpr (F % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < F; k += 4) *reinterpret_cast<float4 *>(a + k) = make_float4(r[k], r[k + 1], r[k + 2], r[k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < F; k += 2) *reinterpret_cast<float2 *>(a + k) = make_float2(r[k], r[k + 1]);
+    }
+}
+
 // One thread per table ENTRY (touched test once; the F contiguous parameters,
 // moments and fixed-point gradients are all loaded before any store, so the
 // loads of a thread overlap) or per MLP parameter.
@@ -370,14 +397,18 @@ __device__ __forceinline__ void adam_entry(const AdamArgs &A, size_t i0) {
     float *__restrict__ M = A.m + i0;
     float *__restrict__ V = A.v + i0;
     unsigned long long *__restrict__ G = A.gtab + i0;
+    // 16-byte vector loads / stores (an entry's F values are F*4-byte
+    // aligned: tables start at 0 and n_pos_tab, entries are F wide)
     unsigned long long gq[F];
     float p[F], m[F], v[F];
+    ld_vec<F>(P, p);
+    ld_vec<F>(M, m);
+    ld_vec<F>(V, v);
 #pragma unroll
-    for (int k = 0; k < F; ++k) {
-        gq[k] = G[k];
-        p[k] = P[k];
-        m[k] = M[k];
-        v[k] = V[k];
+    for (int k = 0; k < F; k += 2) {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(G + k);
+        gq[k] = x.x;
+        gq[k + 1] = x.y;
     }
 #pragma unroll
     for (int k = 0; k < F; ++k) {
@@ -387,12 +418,10 @@ __device__ __forceinline__ void adam_entry(const AdamArgs &A, size_t i0) {
         p[k] -= A.lr * (m[k] / A.bc1) / (sqrtf(v[k] / A.bc2) + A.eps);
     }
 #pragma unroll
-    for (int k = 0; k < F; ++k) {
-        G[k] = 0ull;
-        P[k] = p[k];
-        M[k] = m[k];
-        V[k] = v[k];
-    }
+    for (int k = 0; k < F; k += 2) *reinterpret_cast<ulonglong2 *>(G + k) = make_ulonglong2(0ull, 0ull);
+    st_vec<F>(P, p);
+    st_vec<F>(M, m);
+    st_vec<F>(V, v);
 }
 
 __global__ void k_train_adam(const AdamArgs A, size_t n_pos_entries, size_t n_entries) {
