@@ -50,9 +50,11 @@ __device__ __forceinline__ void st_feats_global(uint8_t *p, const float *acc) {
         __half2 v = __floats2half2_rn(acc[2 * i], acc[2 * i + 1]);
         h[i] = *reinterpret_cast<uint32_t *>(&v);
     }
-    if constexpr (F == 8) *reinterpret_cast<uint4 *>(p) = make_uint4(h[0], h[1], h[2], h[3]);
-    else if constexpr (F == 4) *reinterpret_cast<uint2 *>(p) = make_uint2(h[0], h[1]);
-    else *reinterpret_cast<uint32_t *>(p) = h[0];
+    // streaming stores (evict-first): the 0.9 GB of feature tiles must not
+    // push the level-major encoder's hash tables out of L2
+    if constexpr (F == 8) __stcs(reinterpret_cast<uint4 *>(p), make_uint4(h[0], h[1], h[2], h[3]));
+    else if constexpr (F == 4) __stcs(reinterpret_cast<uint2 *>(p), make_uint2(h[0], h[1]));
+    else __stcs(reinterpret_cast<unsigned int *>(p), h[0]);
 }
 
 // K3: hash-grid encoding, one thread per (query, unit); a warp covers 8
