@@ -148,6 +148,25 @@ class Device {
         check(pf_train_step(ctx_, n, x3, w_sph2, g, targets3, step, total_steps, &loss));
         return loss;
     }
+    // data-parallel train_step: this rank's shard backward, then the caller
+    // all-reduces grad_buffers() in place (int64 SUM, float SUM, uint8 MAX,
+    // e.g. ncclAllReduce on the context's stream), then train_apply().
+    double train_backward(size_t n, const float *x3, const float *w_sph2, const float *g, const float *targets3,
+                          size_t n_global) {
+        double loss_part = 0.0;
+        check(pf_train_backward(ctx_, n, x3, w_sph2, g, targets3, n_global, &loss_part));
+        return loss_part;
+    }
+    struct GradBuffers {
+        void *gtab, *gmlp, *touched;
+        size_t n_tab, n_mlp, n_entries;
+    };
+    GradBuffers grad_buffers() {
+        GradBuffers b{};
+        check(pf_train_grad_buffers(ctx_, &b.gtab, &b.n_tab, &b.gmlp, &b.n_mlp, &b.touched, &b.n_entries));
+        return b;
+    }
+    void train_apply(uint64_t step, uint64_t total_steps) { check(pf_train_apply(ctx_, step, total_steps)); }
     std::vector<double> train(const pf_train_desc &cfg, double *ms_knn = nullptr, double *ms_step = nullptr) {
         std::vector<double> hist(cfg.total_steps);
         check(pf_train(ctx_, &cfg, hist.data(), ms_knn, ms_step, nullptr, nullptr));
