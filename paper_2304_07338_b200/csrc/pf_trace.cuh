@@ -116,7 +116,7 @@ __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3],
 // The persistent render tracer.
 // ---------------------------------------------------------------------------
 template <bool PAR>
-__global__ void __launch_bounds__(PF_TRACE_THREADS, 6)
+__global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
     k_render_trace(const DevScene S, const TraceParams P) {
     using R = typename Prec<PAR>::R;
     using Slot = R;
