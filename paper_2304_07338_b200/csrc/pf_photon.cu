@@ -65,7 +65,7 @@ __device__ __forceinline__ bool track(const DevScene &S, const double o[3], cons
     }
 }
 
-__global__ void __launch_bounds__(128, 6) k_trace_photons(const DevScene S, const PhotonTraceParams P) {
+__global__ void __launch_bounds__(128, 7) k_trace_photons(const DevScene S, const PhotonTraceParams P) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t steps = 0;
     if (i < P.n_total) {
