@@ -88,9 +88,10 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
         float x[3] = {0.f, 0.f, 0.f}, ws[2] = {0.f, 0.f}, gin = 0.f;
         if (valid) {
             if (P.mode == 0) {
-                const HitRec h = P.hits[gr];
-                x[0] = h.x[0], x[1] = h.x[1], x[2] = h.x[2];
-                ws[0] = h.wsph[0], ws[1] = h.wsph[1];
+                // x[3] + wsph[2]: the first 20 bytes of the 32-byte record
+                const float4 a = __ldg(reinterpret_cast<const float4 *>(P.hits + gr));
+                x[0] = a.x, x[1] = a.y, x[2] = a.z;
+                ws[0] = a.w, ws[1] = __ldg(&P.hits[gr].wsph[1]);
                 gin = P.g_render;
             } else {
                 x[0] = P.qx[3 * gr], x[1] = P.qx[3 * gr + 1], x[2] = P.qx[3 * gr + 2];
