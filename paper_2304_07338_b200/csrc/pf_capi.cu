@@ -567,9 +567,9 @@ static int field_load(pf_ctx *c, const FieldDesc &f, const float *params, size_t
 
 // Feature-tile staging budget (HBM): the hit count is only known on the
 // device, so renders launch ceil(n_work / cap) encode+MLP pairs and the
-// surplus pairs exit immediately.  8 GiB keeps C2 (16.6M samples, paper
-// field: 640 B/row) to two pairs.
-static constexpr size_t kFieldStageBytes = (size_t)8 << 30;
+// surplus pairs exit immediately (~11 us each).  12 GiB of the 180 GB keeps
+// C2 (16.6M samples, paper field: 640 B/row = 10.6 GB) to one pair.
+static constexpr size_t kFieldStageBytes = (size_t)12 << 30;
 static constexpr size_t kFieldRowCap = (size_t)1 << 22;
 
 // encode + MLP over n_max items (count on device for renders), in row batches
