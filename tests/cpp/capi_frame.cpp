@@ -68,6 +68,27 @@ int main() {
     double ms_knn = 0, ms_step = 0;
     CHECK(pf_train(ctx, &tr, loss.data(), &ms_knn, &ms_step, nullptr, nullptr));
 
+    // data-parallel step pieces (one rank here): backward of a shard, the
+    // device gradient buffers an NCCL all-reduce would use, Adam
+    {
+        const size_t nb = 512;
+        std::vector<float> x(nb * 3), w(nb * 2), gg(nb), t(nb * 3);
+        for (size_t i = 0; i < nb; ++i) {
+            for (int a = 0; a < 3; ++a) x[3 * i + a] = (float)((i * 37 + a * 11) % 97) / 97.0f;
+            w[2 * i] = (float)(i % 13) / 13.0f;
+            w[2 * i + 1] = (float)(i % 7) / 7.0f;
+            gg[i] = (float)G[i % 3];
+            for (int a = 0; a < 3; ++a) t[3 * i + a] = 0.5f;
+        }
+        double part = -1.0;
+        CHECK(pf_train_backward(ctx, nb, x.data(), w.data(), gg.data(), t.data(), 2 * nb, &part));
+        void *gt = nullptr, *gm = nullptr, *tc = nullptr;
+        size_t nt = 0, nm = 0, ne = 0;
+        CHECK(pf_train_grad_buffers(ctx, &gt, &nt, &gm, &nm, &tc, &ne));
+        if (!gt || !gm || !tc || nt + nm != np || ne == 0 || !(part >= 0.0)) return 3;
+        CHECK(pf_train_apply(ctx, 0, 10));
+    }
+
     // errors come back as status codes + message, never as a CPU fallback
     pf_render_desc bad = d;
     bad.spp = 0;
