@@ -20,6 +20,16 @@
 
 namespace pfk {
 
+// nee_term with omega_out / L_d in the caller's shared-memory columns
+__device__ __forceinline__ void nee_smem(const DevScene &S, int l, const float x[3], float g, float T,
+                                         float (*s_wo)[PF_TRACE_THREADS], float (*s_ld)[PF_TRACE_THREADS], int tx) {
+    const float wo[3] = {s_wo[0][tx], s_wo[1][tx], s_wo[2][tx]};
+    float Ld[3] = {s_ld[0][tx], s_ld[1][tx], s_ld[2][tx]};
+    nee_term<float>(S, l, x, wo, g, T, Ld);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s_ld[c][tx] = Ld[c];
+}
+
 __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const DevScene S, const TraceParams P) {
     float *slots = reinterpret_cast<float *>(P.slots);
     const float ds = S.density_scale_f;
@@ -29,8 +39,13 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
     uint32_t w = 0;
     uint64_t index = 0;
     Pcg rng;
-    float o[3], d[3], wo[3], t = 0.f, t1 = 0.f, tau = 0.f, T = 1.f;
-    float rgba[4], Ld[3];
+    float o[3], d[3], t = 0.f, t1 = 0.f, tau = 0.f, T = 1.f;
+    float sig_s = 0.f;  // sigma_s at the interaction (only the hit record needs it)
+    // per-thread Ld / wo live in shared memory (column per thread, conflict-
+    // free): they are touched once per NEE term, not per tracking step, and
+    // the registers go to the flight state
+    __shared__ float s_ld[3][PF_TRACE_THREADS], s_wo[3][PF_TRACE_THREADS];
+    const int tx = threadIdx.x;
     Dda D;
     int light = 0;
     uint32_t nprim = 0, nshad = 0;
@@ -55,7 +70,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 d[a] *= rl;
-                wo[a] = -d[a];
+                s_wo[a][tx] = -d[a];
             }
             float t0;
             if (!aabb_unit<float>(o, d, 0.0f, __int_as_float(0x7f800000), t0, t1) || !(S.sigma_max_f > 0.0f) ||
@@ -91,11 +106,15 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
             const float sigma = ds * tf_alpha_f(S, scalar);
             if (phase == 1) {
                 if (pcg_u_f(rng) * m < sigma) {
-                    tf_rgba_f(S, scalar, rgba);
+                    {
+                        float rgba[4];
+                        tf_rgba_f(S, scalar, rgba);
+                        sig_s = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) * (1.0f / 3.0f));
+                    }
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         o[a] = x[a];
-                        Ld[a] = 0.f;
+                        s_ld[a][tx] = 0.f;
                     }
                     pcg_init(rng, P.init_nee, index);
                     light = -1;
@@ -120,7 +139,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
         }
         if (!flight_done) continue;
 
-        if (light >= 0) nee_term<float>(S, light, o, wo, g, T, Ld);
+        if (light >= 0) nee_smem(S, light, o, g, T, s_wo, s_ld, tx);
         for (;;) {
             ++light;
             if (light >= S.n_lights) break;
@@ -140,28 +159,28 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
                     break;
                 }
             }
-            nee_term<float>(S, light, o, wo, g, 1.0f, Ld);
+            nee_smem(S, light, o, g, 1.0f, s_wo, s_ld, tx);
         }
         if (light < S.n_lights) continue;
 
         const size_t sb = 3 * (size_t)w;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) slots[sb + c] = (float)P.w_d * Ld[c];
+        for (int c = 0; c < 3; ++c) slots[sb + c] = (float)P.w_d * s_ld[c][tx];
         const unsigned long long h = warp_fetch_add(&P.counters[1], 1u);
         if (P.use_field) {
             HitRec rec;
             rec.x[0] = o[0];
             rec.x[1] = o[1];
             rec.x[2] = o[2];
-            const float wz = fminf(fmaxf(wo[2], -1.0f), 1.0f);
+            const float wz = fminf(fmaxf(s_wo[2][tx], -1.0f), 1.0f);
             rec.wsph[0] = acosf(wz) * (float)(1.0 / kPi);
-            rec.wsph[1] = (atan2f(wo[1], wo[0]) + (float)kPi) * (float)(0.5 / kPi);
+            rec.wsph[1] = (atan2f(s_wo[1][tx], s_wo[0][tx]) + (float)kPi) * (float)(0.5 / kPi);
             rec.slot = w;
-            rec.sigma_s = (double)(rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) * (1.0f / 3.0f)));
+            rec.sigma_s = (double)sig_s;
             P.hits[h] = rec;
             if (P.hit_dir) {
 #pragma unroll
-                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = (double)wo[a];
+                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = (double)s_wo[a][tx];
             }
         }
         phase = 0;
