@@ -42,7 +42,14 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
     Pcg rng;
     R o[3], d[3], pd[3];  // flight origin + direction; pd = direction of the path segment
     R t = 0, t1 = 0, ts0 = 0, T = 1;
-    R rgba[4] = {0, 0, 0, 0}, Ld[3], Ld0[3] = {0, 0, 0}, Li[3] = {0, 0, 0};
+    // radiance accumulators in shared memory (column per thread): touched once
+    // per NEE term / vertex, not per tracking step; [0..2] L_d of the current
+    // vertex, [3..5] L_d of vertex 0, [6..8] L_i
+    __shared__ R s_acc[9][PF_TRACE_THREADS];
+    const int tx = threadIdx.x;
+    R ss_v = 0;  // sigma_s of the current vertex (alpha * mean rgb)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) s_acc[k][tx] = R(0);
     R thr = 1, ss0 = 0;
     int light = 0, trial = 0, passed = 0;
     Dda D;            // FAST only
@@ -64,10 +71,16 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
         }
         return true;
     };
+    auto nee = [&](int l, const R wo[3], R Tl) {
+        R Ld[3] = {s_acc[0][tx], s_acc[1][tx], s_acc[2][tx]};
+        nee_term<R>(S, l, o, wo, g, Tl, Ld);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s_acc[c][tx] = Ld[c];
+    };
     auto finish = [&]() {
         const size_t sb = 3 * (size_t)w;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) slots[sb + c] = (R)P.w_d * Ld0[c] + (R)P.w_i * (ss0 * Li[c]);
+        for (int c = 0; c < 3; ++c) slots[sb + c] = (R)P.w_d * s_acc[3 + c][tx] + (R)P.w_i * (ss0 * s_acc[6 + c][tx]);
         warp_fetch_add(&P.counters[1], 1u);
         phase = 0;
     };
@@ -111,7 +124,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
             vert = 0;
             thr = R(1);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) Li[c] = R(0);
+            for (int c = 0; c < 3; ++c) s_acc[6 + c][tx] = R(0);
             if (!start_flight(R(0), rinf(R(0)))) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = (R)P.bg[c];
@@ -187,11 +200,16 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
                 continue;
             }
             // real interaction: path vertex `vert`
-            tf_rgba(S, scalar, rgba);
+            {
+                R rgba[4];
+                tf_rgba(S, scalar, rgba);
+                if constexpr (PAR) ss_v = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / R(3));
+                else ss_v = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) * (1.0f / 3.0f));
+            }
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 o[a] = x[a];
-                Ld[a] = R(0);
+                s_acc[a][tx] = R(0);
             }
             if (vert == 0) pcg_init(rng, P.init_nee, index);  // vertex 0 lights on the Nee stream
             light = -1;
@@ -207,7 +225,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
                 }
                 T = (R)passed / (R)P.nee_trials;
             }
-            nee_term<R>(S, light, o, wo, g, T, Ld);
+            nee(light, wo, T);
         }
 
         // start the next light's shadow segment x -> P (volume.cpp:230-238)
@@ -229,23 +247,21 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
                     break;
                 }
             }
-            nee_term<R>(S, light, o, wo, g, R(1), Ld);
+            nee(light, wo, R(1));
         }
         if (light < S.n_lights) continue;  // shadow flight started
 
         // ---- vertex lit: accumulate, roulette, scatter --------------------
-        R ss;
-        if constexpr (PAR) ss = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / R(3));
-        else ss = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) * (1.0f / 3.0f));
+        const R ss = ss_v;
         bool go = vert + 1 < P.max_bounces;
         if (vert == 0) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) Ld0[c] = Ld[c];
+            for (int c = 0; c < 3; ++c) s_acc[3 + c][tx] = s_acc[c][tx];
             ss0 = ss;
             if (go) pcg_init(rng, P.init_pt, index);  // the continuation's own stream
         } else {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) Li[c] += thr * Ld[c];
+            for (int c = 0; c < 3; ++c) s_acc[6 + c][tx] += thr * s_acc[c][tx];
             thr *= ss;
             if (go) {
                 if (!(thr > R(0))) {
