@@ -130,8 +130,19 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
     uint32_t w = 0;
     uint64_t index = 0;
     Pcg rng;
-    R o[3], d[3], wo[3], t = 0, t1 = 0, ts0 = 0;
-    R rgba[4], Ld[3];
+    R o[3], d[3], t = 0, t1 = 0, ts0 = 0;
+    R sig_s = 0;  // sigma_s at the interaction (only the hit record needs it)
+    // omega_out / L_d in shared memory (column per thread): touched per NEE
+    // term, not per tracking step
+    __shared__ R s_wo[3][PF_TRACE_THREADS], s_ld[3][PF_TRACE_THREADS];
+    const int tx = threadIdx.x;
+    auto nee = [&](int l, R Tl) {
+        const R wo[3] = {s_wo[0][tx], s_wo[1][tx], s_wo[2][tx]};
+        R Ld[3] = {s_ld[0][tx], s_ld[1][tx], s_ld[2][tx]};
+        nee_term<R>(S, l, o, wo, g, Tl, Ld);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s_ld[c][tx] = Ld[c];
+    };
     int light = 0, trial = 0, passed = 0;
     R T = 1;
     uint32_t nprim = 0, nshad = 0;
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 d[a] = d[a] / len;
-                wo[a] = -d[a];
+                s_wo[a][tx] = -d[a];
             }
             R t0;
             if (!aabb_unit<R>(o, d, R(0), rinf(R(0)), t0, t1) || !(sm > R(0))) {
@@ -195,11 +206,15 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
             if (phase == 1) {
                 if (u2 * sm < sigma) {
                     // real interaction: Interaction{x, scalar, albedo}
-                    tf_rgba(S, scalar, rgba);
+                    {
+                        R rgba[4];
+                        tf_rgba(S, scalar, rgba);
+                        sig_s = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / R(3));
+                    }
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         o[a] = x[a];
-                        Ld[a] = R(0);
+                        s_ld[a][tx] = R(0);
                     }
                     pcg_init(rng, P.init_nee, index);
                     light = -1;
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
                 }
                 T = (R)passed / (R)P.nee_trials;
             }
-            nee_term<R>(S, light, o, wo, g, T, Ld);
+            nee(light, T);
         }
         // start the next light's segment x -> P (volume.cpp:230-238)
         for (;;) {
@@ -263,29 +278,29 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
                     break;
                 }
             }
-            nee_term<R>(S, light, o, wo, g, R(1), Ld);
+            nee(light, R(1));
         }
         if (light < S.n_lights) continue;  // shadow flight started
 
         // ---- all lights done: w_d * L_d into the slot, hit record for the field
         const size_t sb = 3 * (size_t)w;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) slots[sb + c] = (Slot)P.w_d * Ld[c];
+        for (int c = 0; c < 3; ++c) slots[sb + c] = (Slot)P.w_d * s_ld[c][tx];
         if (P.use_field) {
             const unsigned long long h = warp_fetch_add(&P.counters[1], 1u);
             HitRec rec;
             rec.x[0] = (float)o[0];
             rec.x[1] = (float)o[1];
             rec.x[2] = (float)o[2];
-            const float wz = fminf(fmaxf((float)wo[2], -1.0f), 1.0f);
+            const float wz = fminf(fmaxf((float)s_wo[2][tx], -1.0f), 1.0f);
             rec.wsph[0] = acosf(wz) * (float)(1.0 / kPi);
-            rec.wsph[1] = (atan2f((float)wo[1], (float)wo[0]) + (float)kPi) * (float)(0.5 / kPi);
+            rec.wsph[1] = (atan2f((float)s_wo[1][tx], (float)s_wo[0][tx]) + (float)kPi) * (float)(0.5 / kPi);
             rec.slot = w;
-            rec.sigma_s = (double)(rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / R(3)));
+            rec.sigma_s = (double)sig_s;
             P.hits[h] = rec;
             if (P.hit_dir) {
 #pragma unroll
-                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = (double)wo[a];
+                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = (double)s_wo[a][tx];
             }
         } else {
             warp_fetch_add(&P.counters[1], 1u);
