@@ -68,26 +68,30 @@ __device__ __forceinline__ bool track(const DevScene &S, const double o[3], cons
 __global__ void __launch_bounds__(128, 7) k_trace_photons(const DevScene S, const PhotonTraceParams P) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t steps = 0;
+    // per-photon power scale and throughput in shared memory (column per
+    // thread): used once per bounce, so the tracking loop keeps the registers
+    __shared__ double s_scale[3][128], s_thr[3][128];
+    const int tx = threadIdx.x;
     if (i < P.n_total) {
         const uint64_t pairs = (uint64_t)S.n_lights * (uint64_t)P.n_phases;
         const uint64_t pr = i % pairs;
         const int li = (int)(pr / (uint64_t)P.n_phases), gi = (int)(pr % (uint64_t)P.n_phases);
         const double g = P.g[gi];
         const double n_pair = (double)(P.n_total / pairs + (pr < P.n_total % pairs ? 1u : 0u));
-        double scale[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) scale[k] = S.light_i[li][k] / n_pair;
+        for (int k = 0; k < 3; ++k) s_scale[k][tx] = S.light_i[li][k] / n_pair;
         Pcg rng;
         pcg_init(rng, P.initstate, i);
         double o[3] = {S.light_p[li][0], S.light_p[li][1], S.light_p[li][2]}, w[3];
         emit_dir(o, rng, w);
-        double thr[3] = {1.0, 1.0, 1.0};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s_thr[k][tx] = 1.0;
         uint32_t dep = 0;
         for (int bounce = 0; bounce < P.max_bounces; ++bounce) {
             double x[3], c[4];
             if (!track(S, o, w, rng, x, c, steps)) break;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) thr[k] *= c[3] * c[k];
+            for (int k = 0; k < 3; ++k) s_thr[k][tx] *= c[3] * c[k];
             double nw[3];
             {
                 const double u1 = pcg_double(rng), u2 = pcg_double(rng);
@@ -104,7 +108,7 @@ __global__ void __launch_bounds__(128, 7) k_trace_photons(const DevScene S, cons
                     for (int k = 0; k < 3; ++k) {
                         r.pos[k] = (float)x[k];
                         r.dir[k] = (float)nw[k];
-                        r.pow[k] = (float)(scale[k] * thr[k]);
+                        r.pow[k] = (float)(s_scale[k][tx] * s_thr[k][tx]);
                     }
                     r.g_index = (uint8_t)gi;
                     r.pad[0] = (uint8_t)dep;
@@ -115,11 +119,11 @@ __global__ void __launch_bounds__(128, 7) k_trace_photons(const DevScene S, cons
                 ++dep;
             }
             if (bounce >= P.rr_start) {
-                double q = stdmax(stdmax(thr[0], thr[1]), thr[2]);
+                double q = stdmax(stdmax(s_thr[0][tx], s_thr[1][tx]), s_thr[2][tx]);
                 q = q < P.rr_min ? P.rr_min : (q > P.rr_max ? P.rr_max : q);
                 if (pcg_double(rng) >= q) break;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) thr[k] /= q;
+                for (int k = 0; k < 3; ++k) s_thr[k][tx] /= q;
             }
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
