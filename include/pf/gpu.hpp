@@ -79,7 +79,7 @@ class Device {
                                                             bool fp64 = true) {
         const size_t n = rays.size();
         if (idx.size() != n) throw std::invalid_argument("delta_track: idx size mismatch");
-        std::vector<double> o(3 * n), d(3 * n), t0(n), t1(n), pos(3 * n), rgba(4 * n);
+        std::vector<double> o(3 * n), d(3 * n), t0(n), t1(n), pos(3 * n), scalar(n), rgba(4 * n);
         for (size_t i = 0; i < n; ++i) {
             o[3 * i] = rays[i].origin.x, o[3 * i + 1] = rays[i].origin.y, o[3 * i + 2] = rays[i].origin.z;
             d[3 * i] = rays[i].direction.x, d[3 * i + 1] = rays[i].direction.y,
@@ -89,12 +89,13 @@ class Device {
         }
         std::vector<int> hit(n);
         check(pf_delta_track_batch(ctx_, n, o.data(), d.data(), t0.data(), t1.data(), seed, (uint64_t)stream,
-                                   idx.data(), fp64 ? 1 : 0, hit.data(), pos.data(), rgba.data()));
+                                   idx.data(), fp64 ? 1 : 0, hit.data(), pos.data(), scalar.data(), rgba.data()));
         std::vector<std::optional<pf::Interaction>> out(n);
         for (size_t i = 0; i < n; ++i) {
             if (!hit[i]) continue;
             pf::Interaction it;
             it.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            it.scalar = scalar[i];
             it.albedo = {rgba[4 * i], rgba[4 * i + 1], rgba[4 * i + 2], rgba[4 * i + 3]};
             out[i] = it;
         }

@@ -109,6 +109,8 @@ typedef struct {
     uint64_t shadow_steps;   /* tentative collisions, shadow rays */
     float ms_trace, ms_field, ms_compose; /* device time per stage (0 unless timing on) */
     uint32_t kernel_launches;              /* device kernels this call launched */
+    uint64_t voxel_fetches;  /* sigma(x) evaluations actually issued (PARITY: tentative
+                                collisions not settled by the majorant-texture bound) */
 } pf_render_stats;
 
 /* Photon record, pf::Photon (proj/include/pf/photon.hpp:17-22): 40 bytes. */
@@ -221,12 +223,16 @@ int pf_ipc_frame_release(pf_ctx *ctx, void *dev_ptr, int owner);
 
 /* ---- parity entry points: batched pf::delta_track / pf::transmittance --- */
 /* Ray i: origin o3[3i..], unit direction d3[3i..], [tmin, tmax]; its RNG is
- * make_rng(seed, stream, idx[i]).  hit[i] = 1/0, pos3 / rgba4 (may be NULL)
- * receive Interaction::position / albedo.  fp64 = 1: binary64 parity kernel;
- * 0: binary32 fast kernel.  Invalid rays -> PF_ERR_INVALID (volume.cpp:205-207). */
+ * make_rng(seed, stream, idx[i]).  hit[i] = 1/0; pos3 / scalar1 / rgba4 (each
+ * may be NULL) receive Interaction{position, scalar, albedo} (volume.hpp:82-86,
+ * volume.cpp:223).  fp64 = 1: binary64 parity kernel; 0: binary32 fast kernel.
+ * Invalid rays -> PF_ERR_INVALID (volume.cpp:205-207).
+ * Replaces std::optional<Interaction> pf::delta_track(const Medium&, const Ray&,
+ * Pcg32&) (proj/include/pf/volume.hpp:115), one call per ray batch. */
 int pf_delta_track_batch(pf_ctx *ctx, size_t n, const double *o3, const double *d3,
                          const double *tmin, const double *tmax, uint64_t seed, uint64_t stream,
-                         const uint64_t *idx, int fp64, int *hit, double *pos3, double *rgba4);
+                         const uint64_t *idx, int fp64, int *hit, double *pos3, double *scalar1,
+                         double *rgba4);
 /* transmittance(medium, a, b, rng, n_trials) per segment (binary64). */
 int pf_transmittance_batch(pf_ctx *ctx, size_t n, const double *a3, const double *b3,
                            uint64_t seed, uint64_t stream, const uint64_t *idx, int n_trials,

@@ -111,11 +111,12 @@ _SIG = {
     "or_tf_classify": (None, [_P, C.c_double, _P]),
     "or_medium_init": (C.c_int, [_P, _P, _P, C.c_double]),
     "or_delta_track_batch": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_uint64, C.c_uint64, _P,
-                                       _P, _P, _P]),
+                                       _P, _P, _P, _P]),
     "or_transmittance_batch": (None, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64, _P, C.c_int,
                                       _P]),
     "or_rng_doubles": (None, [C.c_uint64, C.c_uint64, C.c_size_t, _P, C.c_int, _P]),
     "or_field_param_count": (C.c_size_t, [_P]),
+    "or_field_init": (None, [_P, C.c_uint64, C.c_double, C.c_double, _P]),
     "or_hashgrid_param_count": (C.c_size_t, [_P]),
     "or_field_input_dim": (C.c_int, [_P]),
     "or_field_encode": (None, [_P, _P, _P, _P, C.c_double, _P]),
@@ -166,7 +167,7 @@ _REF_SIG = {
     "ref_grid_sample": (C.c_double, [_P, _P]),
     "ref_tf_classify": (None, [_P, C.c_double, _P]),
     "ref_delta_track_batch": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_uint64, C.c_uint64,
-                                        _P, _P, _P, _P]),
+                                        _P, _P, _P, _P, _P]),
     "ref_transmittance_batch": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64, _P,
                                           C.c_int, _P]),
     "ref_render_neural": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P]),
@@ -177,10 +178,17 @@ _lib = None
 _ref = None
 
 
+def _stale(out: Path, *srcs: Path) -> bool:
+    if not out.exists():
+        return True
+    have = [p for p in srcs if p.exists()]
+    return bool(have) and out.stat().st_mtime < max(p.stat().st_mtime for p in have)
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
-        if not LIB.exists():
+        if _stale(LIB, HERE / "pf_oracle.c", HERE / "pf_oracle.h"):
             build(ref=False)
         L = C.CDLL(str(LIB))
         for k, (r, a) in _SIG.items():
@@ -197,7 +205,8 @@ def ref_available() -> bool:
 def ref() -> C.CDLL:
     global _ref
     if _ref is None:
-        if not REF_LIB.exists():
+        if not REF_LIB.exists() or ((REF_SRC / "proj").exists() and _stale(
+                REF_LIB, HERE / "ref_shim.cpp", HERE / "pf_oracle.c", HERE / "pf_oracle.h")):
             build(ref=True)
         L = C.CDLL(str(REF_LIB))
         for k, (r, a) in _REF_SIG.items():
@@ -234,7 +243,7 @@ class OracleScene:
     def sigma_max(self) -> float:
         return self.medium.sigma_max
 
-    def delta_track(self, o, d, tmin, tmax, seed, stream, idx):
+    def delta_track(self, o, d, tmin, tmax, seed, stream, idx, with_scalar=False):
         o = np.ascontiguousarray(o, np.float64)
         d = np.ascontiguousarray(d, np.float64)
         tmin = np.ascontiguousarray(tmin, np.float64)
@@ -243,11 +252,12 @@ class OracleScene:
         n = len(idx)
         hit = np.zeros(n, np.int32)
         pos = np.zeros((n, 3))
+        sc = np.zeros(n)
         rgba = np.zeros((n, 4))
         if lib().or_delta_track_batch(C.byref(self.medium), n, _p(o), _p(d), _p(tmin), _p(tmax),
-                                      seed, stream, _p(idx), _p(hit), _p(pos), _p(rgba)):
+                                      seed, stream, _p(idx), _p(hit), _p(pos), _p(sc), _p(rgba)):
             raise ValueError("delta_track: invalid ray")
-        return hit, pos, rgba
+        return (hit, pos, sc, rgba) if with_scalar else (hit, pos, rgba)
 
     def transmittance(self, a, b, seed, stream, idx, n_trials=1):
         a = np.ascontiguousarray(a, np.float64)
@@ -286,7 +296,7 @@ class RefScene:
     def sigma_max(self) -> float:
         return ref().ref_scene_sigma_max(self.h)
 
-    def delta_track(self, o, d, tmin, tmax, seed, stream, idx):
+    def delta_track(self, o, d, tmin, tmax, seed, stream, idx, with_scalar=False):
         o = np.ascontiguousarray(o, np.float64)
         d = np.ascontiguousarray(d, np.float64)
         tmin = np.ascontiguousarray(tmin, np.float64)
@@ -295,11 +305,12 @@ class RefScene:
         n = len(idx)
         hit = np.zeros(n, np.int32)
         pos = np.zeros((n, 3))
+        sc = np.zeros(n)
         rgba = np.zeros((n, 4))
         if ref().ref_delta_track_batch(self.h, n, _p(o), _p(d), _p(tmin), _p(tmax), seed, stream,
-                                       _p(idx), _p(hit), _p(pos), _p(rgba)):
+                                       _p(idx), _p(hit), _p(pos), _p(sc), _p(rgba)):
             raise ValueError(ref().ref_last_error().decode())
-        return hit, pos, rgba
+        return (hit, pos, sc, rgba) if with_scalar else (hit, pos, rgba)
 
     def transmittance(self, a, b, seed, stream, idx, n_trials=1):
         a = np.ascontiguousarray(a, np.float64)
@@ -324,6 +335,14 @@ def field_cfg(fc) -> FieldCfg:
 
 def field_param_count(fc) -> int:
     return lib().or_field_param_count(C.byref(field_cfg(fc)))
+
+
+def field_init(fc, seed=0, embed_scale=1e-4, bias_scale=0.0) -> np.ndarray:
+    """Deterministic parameters in pf_field_init's draw order,
+    computed on the CPU so the reference arm never loads the GPU library."""
+    out = np.empty(field_param_count(fc), np.float32)
+    lib().or_field_init(C.byref(field_cfg(fc)), seed, float(embed_scale), float(bias_scale), _p(out))
+    return out
 
 
 def field_forward(fc, params, x3, w2, g, decoded=False) -> np.ndarray:

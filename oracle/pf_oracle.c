@@ -286,7 +286,7 @@ double or_transmittance(const or_medium *m, const double a[3], const double b[3]
 
 int or_delta_track_batch(const or_medium *m, size_t n, const double *o3, const double *d3,
                          const double *tmin, const double *tmax, uint64_t seed, uint64_t stream,
-                         const uint64_t *idx, int *hit, double *pos3, double *rgba4) {
+                         const uint64_t *idx, int *hit, double *pos3, double *scalar1, double *rgba4) {
     for (size_t i = 0; i < n; ++i) {
         or_pcg32 r;
         or_make_rng(&r, seed, stream, idx[i]);
@@ -295,6 +295,7 @@ int or_delta_track_batch(const or_medium *m, size_t n, const double *o3, const d
         if (h < 0) return -1;
         hit[i] = h;
         if (pos3) memcpy(pos3 + 3 * i, pos, sizeof(pos));
+        if (scalar1) scalar1[i] = h ? s : 0.0;
         if (rgba4) memcpy(rgba4 + 4 * i, rgba, sizeof(rgba));
     }
     return 0;
@@ -442,6 +443,26 @@ static void or_hashgrid_encode(const or_hashgrid_cfg *c, const float *table, con
             for (int k = 0; k < F; ++k) out[l * F + k] += w * (double)e[k];
         }
         off += (size_t)size * F;
+    }
+}
+
+/* Deterministic field init, the same draw order as the
+ * product's pf_field_init: make_rng(seed, FieldInit, 0); tables U(-e, e);
+ * per layer W ~ He-uniform by fan-in, then biases U(-b, b).  Lets the
+ * reference CPU arm build its parameters without the GPU library. */
+void or_field_init(const or_field_cfg *c, uint64_t seed, double embed_scale, double bias_scale,
+                   float *out) {
+    or_pcg32 r;
+    or_make_rng(&r, seed, 6 /* Stream::FieldInit, rng.hpp:68 */, 0);
+    const size_t ntab = or_hashgrid_param_count(&c->pos) + or_hashgrid_param_count(&c->dir);
+    size_t p = 0;
+    for (; p < ntab; ++p) out[p] = (float)((2.0 * or_next_double(&r) - 1.0) * embed_scale);
+    const int din = or_field_input_dim(c);
+    for (int L = 0; L <= c->hidden_layers; ++L) {
+        const int K = L == 0 ? din : c->width, N = L < c->hidden_layers ? c->width : 3;
+        const double a = sqrt(6.0 / K);
+        for (int i = 0; i < N * K; ++i) out[p++] = (float)((2.0 * or_next_double(&r) - 1.0) * a);
+        for (int i = 0; i < N; ++i) out[p++] = (float)((2.0 * or_next_double(&r) - 1.0) * bias_scale);
     }
 }
 

@@ -95,7 +95,7 @@ double or_transmittance(const or_medium *m, const double a[3], const double b[3]
 /* Batched conveniences for the test harness: ray i uses make_rng(seed, stream, idx[i]). */
 int or_delta_track_batch(const or_medium *m, size_t n, const double *o3, const double *d3,
                          const double *tmin, const double *tmax, uint64_t seed, uint64_t stream,
-                         const uint64_t *idx, int *hit, double *pos3, double *rgba4);
+                         const uint64_t *idx, int *hit, double *pos3, double *scalar1, double *rgba4);
 void or_transmittance_batch(const or_medium *m, size_t n, const double *a3, const double *b3,
                             uint64_t seed, uint64_t stream, const uint64_t *idx, int n_trials,
                             double *out);
@@ -125,6 +125,9 @@ uint32_t or_hashgrid_level_size(const or_hashgrid_cfg *c, int l);
 size_t or_hashgrid_param_count(const or_hashgrid_cfg *c);
 int or_field_input_dim(const or_field_cfg *c);
 size_t or_field_param_count(const or_field_cfg *c);
+/* Deterministic init, draw order of pf_field_init. */
+void or_field_init(const or_field_cfg *c, uint64_t seed, double embed_scale, double bias_scale,
+                   float *out);
 /* encode_input -> D_in doubles. */
 void or_field_encode(const or_field_cfg *c, const float *params, const double x[3],
                      const double wsph[2], double g, double *feat);

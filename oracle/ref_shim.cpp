@@ -183,7 +183,7 @@ size_t ref_trace_photons(void *h, const double *lights, int n_lights, uint64_t n
 
 int ref_delta_track_batch(void *h, size_t n, const double *o3, const double *d3,
                           const double *tmin, const double *tmax, uint64_t seed, uint64_t stream,
-                          const uint64_t *idx, int *hit, double *pos3, double *rgba4) {
+                          const uint64_t *idx, int *hit, double *pos3, double *scalar1, double *rgba4) {
     auto *s = static_cast<RefScene *>(h);
     try {
         for (size_t i = 0; i < n; ++i) {
@@ -194,10 +194,12 @@ int ref_delta_track_batch(void *h, size_t n, const double *o3, const double *d3,
                       tmax[i]};
             auto it = pf::delta_track(*s->medium, r, rng);
             hit[i] = it ? 1 : 0;
+            if (scalar1) scalar1[i] = 0.0;
             if (it) {
                 pos3[3 * i] = it->position.x;
                 pos3[3 * i + 1] = it->position.y;
                 pos3[3 * i + 2] = it->position.z;
+                if (scalar1) scalar1[i] = it->scalar;
                 if (rgba4) {
                     rgba4[4 * i] = it->albedo.r;
                     rgba4[4 * i + 1] = it->albedo.g;
@@ -239,9 +241,11 @@ int ref_render_neural(void *h, const or_light *lights, int n_lights, const or_fi
     pf::set_worker_count(workers);
     const size_t rows = (size_t)(rc->y1 - rc->y0);
     const size_t npix = rows * (size_t)(rc->x1 - rc->x0);
-    std::vector<uint64_t> chunk_hits((npix + 63) / 64, 0);
+    // chunks of 4096 samples: 4096 / spp whole pixels
+    const size_t chunk = std::max<size_t>(1, 4096 / (size_t)std::max(1, spp));
+    std::vector<uint64_t> chunk_hits((npix + chunk - 1) / chunk, 0);
     try {
-        pf::parallel_chunks(npix, 64, [&](size_t ci, size_t b, size_t e) {
+        pf::parallel_chunks(npix, chunk, [&](size_t ci, size_t b, size_t e) {
             uint64_t hits = 0;
             for (size_t p = b; p < e; ++p) {
                 const int px = rc->x0 + (int)(p % (size_t)(rc->x1 - rc->x0));

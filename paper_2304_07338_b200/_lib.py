@@ -8,9 +8,12 @@ degrades to a CPU implementation.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libpfgpu.so"
+# PF_LIBPFGPU: load another in-tree build of the same library (A/B of kernel
+# variants in tools/); the default is the package's own libpfgpu.so.
+LIB_PATH = Path(os.environ.get("PF_LIBPFGPU") or Path(__file__).resolve().parent / "libpfgpu.so")
 
 PF_OK, PF_ERR_INVALID, PF_ERR_RUNTIME = 0, 1, 2
 PF_MODE_PARITY, PF_MODE_FAST = 0, 1
@@ -47,7 +50,8 @@ class RenderDesc(C.Structure):
 class RenderStats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("hits", C.c_uint64), ("primary_steps", C.c_uint64),
                 ("shadow_steps", C.c_uint64), ("ms_trace", C.c_float), ("ms_field", C.c_float),
-                ("ms_compose", C.c_float), ("kernel_launches", C.c_uint32)]
+                ("ms_compose", C.c_float), ("kernel_launches", C.c_uint32),
+                ("voxel_fetches", C.c_uint64)]
 
 
 class Photon(C.Structure):
@@ -115,7 +119,7 @@ _SIG = {
     "pf_tiles_unpack": (C.c_int, [_P, C.POINTER(Camera), C.POINTER(RenderDesc), _P, C.c_size_t,
                                   _P]),
     "pf_delta_track_batch": (C.c_int, [_P, C.c_size_t, _P, _P, _P, _P, C.c_uint64, C.c_uint64,
-                                       _P, C.c_int, _P, _P, _P]),
+                                       _P, C.c_int, _P, _P, _P, _P]),
     "pf_transmittance_batch": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64, _P,
                                          C.c_int, _P]),
     "pf_transmittance_ratio_batch": (C.c_int, [_P, C.c_size_t, _P, _P, C.c_uint64, C.c_uint64,

@@ -584,7 +584,10 @@ class Context:
 
     # ---- parity entry points
     def delta_track_batch(self, o3, d3, tmin, tmax, seed: int, stream: str | int, idx,
-                          fp64: bool = True):
+                          fp64: bool = True, with_scalar: bool = False):
+        """pf::delta_track per ray (volume.cpp:204-225) -> (hit, position, albedo), or
+        (hit, position, scalar, albedo) = Interaction{position, scalar, albedo}
+        with with_scalar=True."""
         po, ko = _in(o3, np.float64)
         pd, kd = _in(d3, np.float64)
         p0, k0 = _in(tmin, np.float64)
@@ -594,10 +597,11 @@ class Context:
         ph, hit = _out(None, (n,), np.int32)
         pp, pos = _out(None, (n, 3), np.float64)
         pr, rgba = _out(None, (n, 4), np.float64)
+        psc, scalar = _out(None, (n,), np.float64)
         s = STREAM[stream] if isinstance(stream, str) else int(stream)
         check(lib().pf_delta_track_batch(self._h, n, po, pd, p0, p1, seed, s, pi, int(fp64), ph,
-                                         pp, pr))
-        return hit, pos, rgba
+                                         pp, psc, pr))
+        return (hit, pos, scalar, rgba) if with_scalar else (hit, pos, rgba)
 
     def transmittance_batch(self, a3, b3, seed: int, stream: str | int, idx, n_trials: int = 1,
                             ratio: bool = False):

@@ -150,7 +150,9 @@ struct pf_ctx {
     int atlas_log2 = 0;
     int mc[3] = {0, 0, 0};
     int macro = macro_default();  // voxels per macro-cell edge
-    DevBuf macro_mm, maj, occ;
+    DevBuf macro_mm, maj, maj_hi, occ;
+    cudaArray_t maj_array = nullptr;  // PARITY majorant texture (high words, see DevScene::maj_tex)
+    cudaTextureObject_t maj_tex = 0;
     int nx = 0, ny = 0, nz = 0;
     float vmin = 0.f, vmax = 0.f;
     // medium / lights
@@ -167,7 +169,7 @@ struct pf_ctx {
     size_t f_smem = 0, f_abytes = 32768;
     int sms = 0;
     // render scratch
-    DevBuf slots, hits, hit_dir, counters, frame_stage, stage[8];
+    DevBuf slots, hits, hit_dir, counters, frame_stage, stage[10];
     // knn
     bool has_knn = false;
     KnnParams knn{};
@@ -218,6 +220,7 @@ struct pf_ctx {
         S.atlas = vol_tex;
         S.atlas_log2 = atlas_log2;
         S.maj = (const float *)maj.p;
+        S.maj_tex = maj_tex;
         S.occ = (const int *)occ.p;
         for (int a = 0; a < 3; ++a) {
             const int n = a == 0 ? nx : a == 1 ? ny : nz;
@@ -254,8 +257,12 @@ struct pf_ctx {
     void free_volume() {
         if (vol_tex) cudaDestroyTextureObject(vol_tex);
         if (vol_array) cudaFreeArray(vol_array);
+        if (maj_tex) cudaDestroyTextureObject(maj_tex);
+        if (maj_array) cudaFreeArray(maj_array);
         vol_tex = 0;
         vol_array = nullptr;
+        maj_tex = 0;
+        maj_array = nullptr;
         nx = ny = nz = 0;
     }
 };
@@ -358,8 +365,11 @@ int pf_volume_upload(pf_ctx *c, int nx, int ny, int nz, const float *data) {
     const float *src = data;
     const bool dev = is_device_ptr(data);
     if (dev) {
+        // ordered on the context stream (not the legacy default stream, which
+        // does not wait for non-blocking streams such as a torch side stream)
         host.resize(n);
-        PF_CUDA(cudaMemcpy(host.data(), data, n * 4, cudaMemcpyDeviceToHost));
+        PF_CUDA(cudaMemcpyAsync(host.data(), data, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        PF_CUDA(cudaStreamSynchronize(c->stream));
         src = host.data();
     }
     // VolumeGrid ctor validation + attained range (volume.cpp:24-39)
@@ -391,6 +401,7 @@ int pf_volume_upload(pf_ctx *c, int nx, int ny, int nz, const float *data) {
     const size_t ncell = (size_t)c->mc[0] * c->mc[1] * c->mc[2];
     PF_CUDA(c->macro_mm.ensure(ncell * sizeof(float2)));
     PF_CUDA(c->maj.ensure(ncell * sizeof(float)));
+    PF_CUDA(c->maj_hi.ensure(ncell * sizeof(uint32_t)));
     PF_CUDA(launch_macro_minmax((const float *)lin.p, nx, ny, nz, (float2 *)c->macro_mm.p, c->mc[0], c->mc[1],
                                 c->mc[2], c->macro, c->stream));
     cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
@@ -409,6 +420,21 @@ int pf_volume_upload(pf_ctx *c, int nx, int ny, int nz, const float *data) {
     td.readMode = cudaReadModeElementType;
     td.normalizedCoords = 0;
     PF_CUDA(cudaCreateTextureObject(&c->vol_tex, &rd, &td, nullptr));
+    {  // PARITY majorant texture: mc[0] x mc[1] x mc[2] uint32, point-sampled, clamped
+        cudaChannelFormatDesc md = cudaCreateChannelDesc<unsigned int>();
+        PF_CUDA(cudaMalloc3DArray(&c->maj_array, &md, make_cudaExtent(c->mc[0], c->mc[1], c->mc[2])));
+        cudaResourceDesc mr;
+        std::memset(&mr, 0, sizeof(mr));
+        mr.resType = cudaResourceTypeArray;
+        mr.res.array.array = c->maj_array;
+        cudaTextureDesc mt;
+        std::memset(&mt, 0, sizeof(mt));
+        mt.addressMode[0] = mt.addressMode[1] = mt.addressMode[2] = cudaAddressModeClamp;
+        mt.filterMode = cudaFilterModePoint;
+        mt.readMode = cudaReadModeElementType;
+        mt.normalizedCoords = 0;
+        PF_CUDA(cudaCreateTextureObject(&c->maj_tex, &mr, &mt, nullptr));
+    }
     c->atlas_log2 = lg;
     c->nx = nx;
     c->ny = ny;
@@ -458,7 +484,17 @@ int pf_medium_set(pf_ctx *c, const double *tf_pts, int n_pts, double density_sca
     std::memcpy(tp.p, c->tf.data(), c->tf.size() * sizeof(double));
     PF_CUDA(c->occ.ensure(6 * sizeof(int)));
     PF_CUDA(launch_macro_majorant((const float2 *)c->macro_mm.p, (size_t)c->mc[0] * c->mc[1] * c->mc[2], tp, n_pts,
-                                  density_scale, (float *)c->maj.p, c->mc[0], c->mc[1], (int *)c->occ.p, c->stream));
+                                  density_scale, (float *)c->maj.p, (uint32_t *)c->maj_hi.p, c->mc[0], c->mc[1],
+                                  (int *)c->occ.p, c->stream));
+    {
+        cudaMemcpy3DParms cp;
+        std::memset(&cp, 0, sizeof(cp));
+        cp.srcPtr = make_cudaPitchedPtr(c->maj_hi.p, (size_t)c->mc[0] * 4, c->mc[0], c->mc[1]);
+        cp.dstArray = c->maj_array;
+        cp.extent = make_cudaExtent(c->mc[0], c->mc[1], c->mc[2]);
+        cp.kind = cudaMemcpyDeviceToDevice;
+        PF_CUDA(cudaMemcpy3DAsync(&cp, c->stream));
+    }
     c->has_medium = true;
     return PF_OK;
 }
@@ -538,7 +574,8 @@ static int field_load(pf_ctx *c, const FieldDesc &f, const float *params, size_t
     const float *src = params;
     if (is_device_ptr(params)) {
         host.resize(n);
-        PF_CUDA(cudaMemcpy(host.data(), params, n * 4, cudaMemcpyDeviceToHost));
+        PF_CUDA(cudaMemcpyAsync(host.data(), params, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        PF_CUDA(cudaStreamSynchronize(c->stream));
         src = host.data();
     }
     for (size_t i = 0; i < n; ++i)
@@ -854,7 +891,7 @@ static int render_common(pf_ctx *c, const pf_camera *cam, const pf_render_desc *
         PF_CUDA(cudaMemcpyAsync(out_rgb, frame, (size_t)cam->width * cam->height * 12, cudaMemcpyDeviceToHost,
                                 c->stream));
     if (stats) {
-        unsigned long long cnt[4];
+        unsigned long long cnt[5];
         PF_CUDA(cudaMemcpyAsync(cnt, c->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
         PF_CUDA(cudaStreamSynchronize(c->stream));
         std::memset(stats, 0, sizeof(*stats));
@@ -862,6 +899,7 @@ static int render_common(pf_ctx *c, const pf_camera *cam, const pf_render_desc *
         stats->hits = cnt[1];
         stats->primary_steps = cnt[2];
         stats->shadow_steps = cnt[3];
+        stats->voxel_fetches = cnt[4];
         // samples = work items that map into the frame
         uint64_t samples = 0;
         {
@@ -986,7 +1024,7 @@ static int batch_common(pf_ctx *c, size_t n, const double *a3, const double *b3,
 
 int pf_delta_track_batch(pf_ctx *c, size_t n, const double *o3, const double *d3, const double *tmin,
                          const double *tmax, uint64_t seed, uint64_t stream, const uint64_t *idx, int fp64,
-                         int *hit, double *pos3, double *rgba4) {
+                         int *hit, double *pos3, double *scalar1, double *rgba4) {
     if (!c || (n && (!o3 || !d3 || !tmin || !tmax || !idx || !hit)))
         return set_err(PF_ERR_INVALID, "pf_delta_track_batch: null argument");
     if (!c->vol_tex || !c->has_medium) return set_err(PF_ERR_INVALID, "delta_track: volume/medium not set");
@@ -999,7 +1037,8 @@ int pf_delta_track_batch(pf_ctx *c, size_t n, const double *o3, const double *d3
         auto fetch = [&](const double *p, size_t cnt, std::vector<double> &v) -> const double * {
             if (!is_device_ptr(p)) return p;
             v.resize(cnt);
-            cudaMemcpy(v.data(), p, cnt * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpyAsync(v.data(), p, cnt * 8, cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
             return v.data();
         };
         po = fetch(o3, 3 * n, ho);
@@ -1020,20 +1059,23 @@ int pf_delta_track_batch(pf_ctx *c, size_t n, const double *o3, const double *d3
     B.tmin = (const double *)dmin;
     B.tmax = (const double *)dmax;
     B.initstate = stream_initstate(seed, stream);
-    void *dhit, *dpos = nullptr, *drgba = nullptr;
-    bool hh, hp = false, hr = false;
+    void *dhit, *dpos = nullptr, *drgba = nullptr, *dsc = nullptr;
+    bool hh, hp = false, hr = false, hs = false;
     PF_CUDA(c->out_ptr(5, hit, n * 4, &dhit, &hh));
     if (pos3) PF_CUDA(c->out_ptr(6, pos3, n * 24, &dpos, &hp));
     if (rgba4) PF_CUDA(c->out_ptr(7, rgba4, n * 32, &drgba, &hr));
+    if (scalar1) PF_CUDA(c->out_ptr(8, scalar1, n * 8, &dsc, &hs));
     B.hit = (int *)dhit;
     B.pos3 = (double *)dpos;
     B.rgba4 = (double *)drgba;
+    B.scalar = (double *)dsc;
     const DevScene S = c->scene();
     PF_CUDA(fp64 ? launch_delta_track_batch_parity(S, B, c->stream) : launch_delta_track_batch_fast(S, B, c->stream));
     if (hh) PF_CUDA(cudaMemcpyAsync(hit, dhit, n * 4, cudaMemcpyDeviceToHost, c->stream));
     if (hp) PF_CUDA(cudaMemcpyAsync(pos3, dpos, n * 24, cudaMemcpyDeviceToHost, c->stream));
     if (hr) PF_CUDA(cudaMemcpyAsync(rgba4, drgba, n * 32, cudaMemcpyDeviceToHost, c->stream));
-    if (hh || hp || hr) PF_CUDA(cudaStreamSynchronize(c->stream));
+    if (hs) PF_CUDA(cudaMemcpyAsync(scalar1, dsc, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (hh || hp || hr || hs) PF_CUDA(cudaStreamSynchronize(c->stream));
     return PF_OK;
 }
 

@@ -134,7 +134,7 @@ __device__ double tf_alpha_host_like(const TfPoints &T, int n, double s) {
 }
 
 __global__ void k_macro_majorant(const float2 *mm, size_t ncells, const TfPoints T, int n, double ds, float *maj,
-                                 int mcx, int mcy, int *occ) {
+                                 uint32_t *maj_hi, int mcx, int mcy, int *occ) {
     const double *tf = T.p;
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncells) return;
@@ -142,7 +142,11 @@ __global__ void k_macro_majorant(const float2 *mm, size_t ncells, const TfPoints
     double m = fmax(tf_alpha_host_like(T, n, lo), tf_alpha_host_like(T, n, hi));
     for (int i = 0; i < n; ++i)
         if (tf[5 * i] > lo && tf[5 * i] < hi) m = fmax(m, tf[5 * i + 4]);
-    maj[c] = m > 0.0 ? (float)(ds * m * (1.0 + 1e-5)) : 0.0f;
+    const float b = m > 0.0 ? (float)(ds * m * (1.0 + 1e-5)) : 0.0f;
+    maj[c] = b;
+    // high word of (double)b, rounded up: as_double(hi, 0) >= b
+    const unsigned long long bits = (unsigned long long)__double_as_longlong((double)b);
+    maj_hi[c] = (uint32_t)(bits >> 32) + ((uint32_t)bits != 0u ? 1u : 0u);
     if (m > 0.0) {  // occupied-cell bounding box
         const int cx = (int)(c % (size_t)mcx), cy = (int)((c / (size_t)mcx) % (size_t)mcy),
                   cz = (int)(c / ((size_t)mcx * (size_t)mcy));
@@ -163,12 +167,13 @@ cudaError_t launch_macro_minmax(const float *vol, int nx, int ny, int nz, float2
 }
 
 cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const TfPoints &tf_pts, int n_tf, double ds,
-                                  float *maj, int mcx, int mcy, int *occ, cudaStream_t st) {
+                                  float *maj, uint32_t *maj_hi, int mcx, int mcy, int *occ, cudaStream_t st) {
     // occ = {INT_MAX-ish x3, -1 x3} before the min / max reduction
     cudaError_t e = cudaMemsetAsync(occ, 0x7f, 3 * sizeof(int), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(occ + 3, 0xff, 3 * sizeof(int), st);
     if (e != cudaSuccess) return e;
-    k_macro_majorant<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(mm, ncells, tf_pts, n_tf, ds, maj, mcx, mcy, occ);
+    k_macro_majorant<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(mm, ncells, tf_pts, n_tf, ds, maj, maj_hi, mcx, mcy,
+                                                                      occ);
     return cudaGetLastError();
 }
 

@@ -56,6 +56,13 @@ struct DevScene {
     const int *occ;
     int mc[3];
     float mh[3], minv_h[3];
+    // PARITY mode: the same majorants as a point-sampled 3-D texture of the
+    // high 32 bits of each bound as a binary64, rounded up (so
+    // as_double(hi, 0) >= maj).  For u2*sigma_max >= 0 the certain-null test
+    // u2*sigma_max >= bound is then one integer compare of high words, and
+    // the hardware does the cell lookup (floor + clamp) from float
+    // coordinates x * minv_h (pf_parstep.cuh).
+    cudaTextureObject_t maj_tex;
 };
 
 // ------------------------------------------------------------------ rng --

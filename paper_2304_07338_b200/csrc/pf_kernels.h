@@ -71,6 +71,7 @@ struct BatchParams {
     int n_trials;
     int *hit;
     double *pos3, *rgba4, *out;
+    double *scalar;  // Interaction::scalar (volume.hpp:82-86), optional
 };
 
 // Per-pixel compose over the spp slots (K5) + tile helpers.
@@ -103,7 +104,8 @@ struct TfPoints {
     double p[16 * 5];
 };
 cudaError_t launch_macro_majorant(const float2 *mm, size_t ncells, const TfPoints &tf_pts, int n_tf,
-                                  double density_scale, float *maj, int mcx, int mcy, int *occ, cudaStream_t st);
+                                  double density_scale, float *maj, uint32_t *maj_hi, int mcx, int mcy, int *occ,
+                                  cudaStream_t st);
 cudaError_t launch_build_atlas(const float *vol, int nx, int ny, int nz, int log2_cols, float *atlas,
                                size_t aw, size_t ah, cudaStream_t st);
 

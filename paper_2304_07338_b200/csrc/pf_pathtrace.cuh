@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
     for (int k = 0; k < 9; ++k) s_acc[k][tx] = R(0);
     R thr = 1, ss0 = 0;
     int light = 0, trial = 0, passed = 0;
+    ParFlight F;      // PARITY only: majorant-texture coordinates of the flight (origin at tb)
+    R tb = 0;         // PARITY only: flight segment start
     Dda D;            // FAST only
     float tau = 0.f;  // FAST only
     uint32_t nprim = 0, nshad = 0;
@@ -65,7 +67,10 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
         }
         t = a0;
         t1 = a1;
-        if constexpr (!PAR) {
+        if constexpr (PAR) {
+            tb = a0;
+            par_flight(S, o, d, a0, F);  // majorant-texture coordinates (pf_parstep.cuh)
+        } else {
             dda_init(S, o, d, t, D);
             tau = sample_tau(rng);
         }
@@ -143,12 +148,12 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PAR ? 6 : 8) k_render_pt(con
             if (t > t1) {
                 left = true;
             } else {
+                const double u2sm = par_u2sm(rng, (double)sm * 0x1.0p-53);
+                if (par_certain_null(S, F, t, tb, u2sm)) continue;  // certain null collision
 #pragma unroll
                 for (int a = 0; a < 3; ++a) x[a] = o[a] + d[a] * t;
-                const R u2 = uniform(rng, R(0));
-                if (u2 * sm >= (R)cell_bound(S, x)) continue;  // certain null collision
                 scalar = sample(S, x);
-                if (!(u2 * sm < ds * tf_alpha(S, scalar))) continue;  // null collision
+                if (!(u2sm < ds * tf_alpha(S, scalar))) continue;  // null collision
             }
         } else {
             float m;

@@ -49,19 +49,21 @@ __device__ __forceinline__ bool track(const DevScene &S, const double o[3], cons
     double t0, t1;
     if (!aabb_unit<double>(o, d, 0.0, rinf(0.0), t0, t1)) return false;
     if (S.sigma_max <= 0.0) return false;
-    const double inv = S.inv_sigma_max;
+    const double inv = S.inv_sigma_max, sm53 = S.sigma_max * 0x1.0p-53;
+    ParFlight F;
+    par_flight(S, o, d, t0, F);
     double t = t0;
     for (;;) {
-        t -= log(1.0 - pcg_double(rng)) * inv;
+        t -= par_step(rng, inv);
         if (t > t1) return false;
         ++steps;
+        const double u2sm = par_u2sm(rng, sm53);
+        if (par_certain_null(S, F, t, t0, u2sm)) continue;
 #pragma unroll
         for (int a = 0; a < 3; ++a) x[a] = o[a] + d[a] * t;
-        const double u2 = pcg_double(rng);
-        if (u2 * S.sigma_max >= cell_bound(S, x)) continue;
         const double s = sample_d(S, x);
         tf_rgba_d(S, s, c);
-        if (u2 * S.sigma_max < S.density_scale * c[3]) return true;
+        if (u2sm < S.density_scale * c[3]) return true;
     }
 }
 

@@ -1,11 +1,13 @@
 // pf_trace.cuh -- K1/K2: persistent primary delta tracking + NEE shadow rays.
 //
-// One template, two translation units:
-//   pf_trace_parity.cu (PF_PAR = true,  binary64, --fmad=false) reproduces
-//     pf::delta_track / pf::transmittance (proj/src/volume.cpp:204-256)
-//     operation-for-operation with the same RNG consumption;
-//   pf_trace_fast.cu   (PF_PAR = false, binary32) is the throughput mode:
-//     same streams (2 x u32 per uniform), ratio-tracked shadow rays.
+// Included by two translation units:
+//   pf_trace_parity.cu (binary64, --fmad=false): k_render_trace_parity and the
+//     batch entry points reproduce pf::delta_track / pf::transmittance
+//     (proj/src/volume.cpp:204-256) operation-for-operation with the same RNG
+//     consumption (tracking step: pf_parstep.cuh);
+//   pf_trace_fast.cu (binary32): the throughput mode (own kernel), same
+//     streams (2 x u32 per uniform), macro-cell DDA + ratio-tracked shadow rays;
+//     it uses the precision-dispatched primitives below.
 //
 // Design (B200): a persistent grid (resident CTAs = SM count x occupancy)
 // where every lane is a small state machine {fetch sample, primary flight,
@@ -19,6 +21,7 @@
 
 #include "pf_device.cuh"
 #include "pf_kernels.h"
+#include "pf_parstep.cuh"
 
 namespace pfk {
 
@@ -54,7 +57,7 @@ __device__ __forceinline__ bool decode_work(const TraceParams &P, uint32_t w, in
 
 // ----- precision-dispatched primitives ------------------------------------
 __device__ __forceinline__ double step_len(Pcg &r, double inv) {
-    return log(1.0 - pcg_double(r)) * inv;  // volume.cpp:217 / 247
+    return pf_log(1.0 - pcg_double(r)) * inv;  // volume.cpp:217 / 247 (pf_log.h)
 }
 __device__ __forceinline__ float step_len(Pcg &r, float inv) {
     return __logf(pcg_one_minus_u_f(r)) * inv;
@@ -78,22 +81,6 @@ __device__ __forceinline__ float rsqrt_len(float v) { return sqrtf(v); }
 __device__ __forceinline__ double rinf(double) { return __longlong_as_double(0x7ff0000000000000ll); }
 __device__ __forceinline__ float rinf(float) { return __int_as_float(0x7f800000); }
 
-// Conservative bound on sigma(x) from the macro-cell majorant grid: every
-// trilinear sample inside the cell is covered (cell support +-1 voxel), so
-// u2 * sigma_max >= bound implies the reference rejects the tentative
-// collision (volume.cpp:222-223).  Used to skip the fetch + classify of
-// certain null collisions WITHOUT changing the RNG sequence or any decision.
-__device__ __forceinline__ double cell_bound(const DevScene &S, const double x[3]) {
-    int c[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        // fmax/fmin also map NaN to a valid cell (the bound is then just looser)
-        const double p = fmin(fmax(x[a] * (double)S.minv_h[a], 0.0), (double)(S.mc[a] - 1));
-        c[a] = (int)p;
-    }
-    return (double)__ldg(S.maj + c[0] + S.mc[0] * (c[1] + S.mc[1] * c[2]));
-}
-
 // One light's NEE term (pinned: oracle/pf_oracle.c or_nee_term).
 template <typename R>
 __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3], const R wo[3], R g,
@@ -112,251 +99,322 @@ __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3],
     for (int ch = 0; ch < 3; ++ch) Ld[ch] += s * (R)S.light_i[l][ch];
 }
 
+#ifdef PF_TU_PARITY  // kernels defined in pf_trace_parity.cu only
 // ---------------------------------------------------------------------------
-// The persistent render tracer.
+// The persistent PARITY render tracer (binary64, the reference's global
+// majorant and RNG consumption; the FAST tracer is pf_trace_fast.cu).
+// Per lane: {fetch sample -> primary flight -> shadow flight(s) per light}.
+// The tracking step (pf_parstep.cuh) only touches the RNG state, t, and six
+// float majorant-texture coordinates; the binary64 ray (origin, direction),
+// omega_out, L_d and the sample index live in per-thread shared-memory
+// columns and are read only at events (a voxel fetch, a flight end), which
+// keeps the step loop spill-free and short (~100 instructions vs ~280).
 // ---------------------------------------------------------------------------
-template <bool PAR>
-__global__ void __launch_bounds__(PF_TRACE_THREADS, 7)
-    k_render_trace(const DevScene S, const TraceParams P) {
-    using R = typename Prec<PAR>::R;
-    using Slot = R;
-    Slot *slots = reinterpret_cast<Slot *>(P.slots);
-    const R inv_sm = inv_majorant(S, R(0));
-    const R sm = majorant(S, R(0));
-    const R ds = density(S, R(0));
-    const R g = (R)P.g;
+#ifndef PF_PAR_REFILL
+#define PF_PAR_REFILL 28  // waiting lanes that trigger a warp-wide refill
+#endif
+#ifndef PF_PAR_FETCH
+#define PF_PAR_FETCH 4  // lanes parked at a voxel fetch that trigger a fetch round
+#endif
+#ifndef PF_PAR_CTAS
+#define PF_PAR_CTAS 7  // resident CTAs per SM (register budget 65536 / (128 x 7) = 73)
+#endif
+__global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
+    k_render_trace_parity(const DevScene S, const TraceParams P) {
+    double *slots = reinterpret_cast<double *>(P.slots);
+    const double inv_sm = S.inv_sigma_max;
+    const double sm = S.sigma_max;
+    const double sm53 = S.sigma_max * 0x1.0p-53;
+    const double ds = S.density_scale;
+    const double g = P.g;
 
-    int phase = 0;  // 0 fetch, 1 primary flight, 2 shadow flight
-    uint32_t w = 0;
-    uint64_t index = 0;
-    Pcg rng;
-    R o[3], d[3], t = 0, t1 = 0, ts0 = 0;
-    R sig_s = 0;  // sigma_s at the interaction (only the hit record needs it)
-    // omega_out / L_d in shared memory (column per thread): touched per NEE
-    // term, not per tracking step
-    __shared__ R s_wo[3][PF_TRACE_THREADS], s_ld[3][PF_TRACE_THREADS];
+    // event-only state: per-thread shared-memory columns
+    __shared__ double s_o[3][PF_TRACE_THREADS], s_d[3][PF_TRACE_THREADS];
+    __shared__ double s_wo[3][PF_TRACE_THREADS], s_ld[3][PF_TRACE_THREADS];
+    __shared__ double s_sig[PF_TRACE_THREADS], s_tb[PF_TRACE_THREADS];
+    __shared__ unsigned long long s_idx[PF_TRACE_THREADS];
+    __shared__ uint32_t s_w[PF_TRACE_THREADS];
+    __shared__ int s_light[PF_TRACE_THREADS], s_trial[PF_TRACE_THREADS], s_passed[PF_TRACE_THREADS];
+    // shadow-step accounting without a second per-step counter: nstep at the
+    // start of the current shadow flight, and the shadow steps so far
+    __shared__ uint32_t s_mark[PF_TRACE_THREADS], s_nshad[PF_TRACE_THREADS];
+    __shared__ double s_u2[PF_TRACE_THREADS];      // u2 * sigma_max of a parked lane
+    __shared__ uint32_t s_nfetch[PF_TRACE_THREADS];  // voxel fetches (sigma(x) evaluations)
+    __shared__ float4 s_qa[PF_TRACE_THREADS];
+    __shared__ float2 s_qb[PF_TRACE_THREADS];
+    const ParFlightSmem Fm{s_qa, s_qb};
     const int tx = threadIdx.x;
-    auto nee = [&](int l, R Tl) {
-        const R wo[3] = {s_wo[0][tx], s_wo[1][tx], s_wo[2][tx]};
-        R Ld[3] = {s_ld[0][tx], s_ld[1][tx], s_ld[2][tx]};
-        nee_term<R>(S, l, o, wo, g, Tl, Ld);
+
+    // step-loop state: registers
+    // 0 waiting for a sample, 1 primary flight, 2 shadow flight, 3 queue drained;
+    // | 4: parked at a voxel fetch (sigma(x) pending) of a primary / shadow flight
+    int phase = 0;
+    Pcg rng;
+    double t = 0, t1 = 0;
+    uint32_t nstep = 0;
+    s_nshad[tx] = 0;
+    s_nfetch[tx] = 0;
+
+    auto nee = [&](int l, double Tl) {
+        const double x[3] = {s_o[0][tx], s_o[1][tx], s_o[2][tx]};
+        const double wo[3] = {s_wo[0][tx], s_wo[1][tx], s_wo[2][tx]};
+        double Ld[3] = {s_ld[0][tx], s_ld[1][tx], s_ld[2][tx]};
+        nee_term<double>(S, l, x, wo, g, Tl, Ld);
 #pragma unroll
         for (int c = 0; c < 3; ++c) s_ld[c][tx] = Ld[c];
     };
-    int light = 0, trial = 0, passed = 0;
-    R T = 1;
-    uint32_t nprim = 0, nshad = 0;
 
+    // Lanes whose sample ended wait (phase 0) until PF_PAR_REFILL lanes of the
+    // warp are waiting (or none is tracking), then refill together: the
+    // ~300-instruction sample setup (work decode, camera ray, 6 binary64
+    // divisions, box clip) then runs once per group instead of once per lane
+    // with 1-2 lanes active (profiles/r02b_*: 25% of the kernel's instructions).
     for (;;) {
-        if (phase == 0) {
-            w = (uint32_t)warp_fetch_add(&P.counters[0], 1u);
-            if (w >= P.n_work) break;
-            int px, py;
-            if (!decode_work(P, w, px, py, index)) continue;
-            pcg_init(rng, P.init_cam, index);
-            const double u = pcg_double(rng);
-            const double v = pcg_double(rng);
-            // pinned camera (oracle or_camera_ray)
-            const R sx = (R(2) * ((R)px + (R)u)) / (R)P.W - R(1);
-            const R sy = R(1) - (R(2) * ((R)py + (R)v)) / (R)P.H;
+        const unsigned waiting = __ballot_sync(0xffffffffu, phase == 0);
+        const unsigned tracking = __ballot_sync(0xffffffffu, phase == 1 || phase == 2);
+        const unsigned parked = __ballot_sync(0xffffffffu, (phase & 4) != 0);
+        if (waiting && (tracking == 0 || __popc(waiting) >= PF_PAR_REFILL)) {
+            while (phase == 0) {
+                const uint32_t w = (uint32_t)warp_fetch_add(&P.counters[0], 1u);
+                if (w >= P.n_work) {
+                    phase = 3;  // queue drained
+                    break;
+                }
+                int px, py;
+                uint64_t index;
+                if (!decode_work(P, w, px, py, index)) continue;
+                s_w[tx] = w;
+                s_idx[tx] = index;
+                pcg_init(rng, P.init_cam, index);
+                const double u = pcg_double(rng);
+                const double v = pcg_double(rng);
+                // pinned camera (oracle or_camera_ray)
+                const double sx = (2.0 * ((double)px + u)) / (double)P.W - 1.0;
+                const double sy = 1.0 - (2.0 * ((double)py + v)) / (double)P.H;
+                double o[3], d[3];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                o[a] = (R)P.cam_o[a];
-                d[a] = ((R)P.cam_f[a] + (R)P.cam_r[a] * sx) + (R)P.cam_u[a] * sy;
-            }
-            const R len = rsqrt_len(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+                for (int a = 0; a < 3; ++a) {
+                    o[a] = P.cam_o[a];
+                    d[a] = (P.cam_f[a] + P.cam_r[a] * sx) + P.cam_u[a] * sy;
+                }
+                const double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                d[a] = d[a] / len;
-                s_wo[a][tx] = -d[a];
-            }
-            R t0;
-            if (!aabb_unit<R>(o, d, R(0), rinf(R(0)), t0, t1) || !(sm > R(0))) {
+                for (int a = 0; a < 3; ++a) {
+                    d[a] = d[a] / len;
+                    s_wo[a][tx] = -d[a];
+                    s_o[a][tx] = o[a];
+                    s_d[a][tx] = d[a];
+                }
+                double t0;
+                if (!aabb_unit<double>(o, d, 0.0, rinf(0.0), t0, t1) || !(sm > 0.0)) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = (Slot)P.bg[c];
-                continue;
+                    for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = P.bg[c];
+                    continue;
+                }
+                t = t0;
+                s_tb[tx] = t0;
+                {
+                    ParFlight F;
+                    par_flight(S, o, d, t0, F);
+                    par_store(Fm, tx, F);
+                }
+                phase = 1;
             }
-            t = t0;
-            phase = 1;
+            continue;  // re-evaluate the warp's state
         }
-
-        // ---- one tentative-collision step (shared by both flight kinds) ----
-        t -= step_len(rng, inv_sm);
-        if (phase == 1) ++nprim;
-        else ++nshad;
+        if (tracking == 0 && parked == 0) break;  // every lane drained
 
         bool flight_done = false;  // shadow flight finished this step
         bool collided = false;
-        if (t > t1) {
-            if (phase == 1) {  // primary ray left the volume: background
+        if (parked && (tracking == 0 || __popc(parked) >= PF_PAR_FETCH)) {
+            // ---- fetch round: the parked lanes evaluate sigma(x) together ----
+            if ((phase & 4) == 0) continue;
+            phase &= 3;
+            ++s_nfetch[tx];
+            const double u2sm = s_u2[tx];
+            double x[3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = (Slot)P.bg[c];
-                phase = 0;
-                continue;
-            }
-            flight_done = true;
-        } else {
-            R x[3] = {o[0] + d[0] * t, o[1] + d[1] * t, o[2] + d[2] * t};
-            // u2 is drawn before sigma(x) is evaluated: nothing else touches the
-            // stream in between, so the sequence is the reference's
-            const R u2 = uniform(rng, R(0));
-            if (u2 * sm >= (R)cell_bound(S, x)) continue;  // certain null collision
-            const R scalar = sample(S, x);
-            const R sigma = ds * tf_alpha(S, scalar);
-            if (phase == 1) {
-                if (u2 * sm < sigma) {
+            for (int a = 0; a < 3; ++a) x[a] = s_o[a][tx] + s_d[a][tx] * t;  // ray.at(t)
+            const double scalar = sample_d(S, x);
+            const double sigma = ds * tf_alpha_d(S, scalar);
+            if (!(u2sm < sigma)) continue;  // null collision: back to stepping
+            {
+                if (phase == 1) {
                     // real interaction: Interaction{x, scalar, albedo}
-                    {
-                        R rgba[4];
-                        tf_rgba(S, scalar, rgba);
-                        sig_s = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / R(3));
-                    }
+                    double rgba[4];
+                    tf_rgba_d(S, scalar, rgba);
+                    s_sig[tx] = rgba[3] * ((rgba[0] + rgba[1] + rgba[2]) / 3.0);
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
-                        o[a] = x[a];
-                        s_ld[a][tx] = R(0);
+                        s_o[a][tx] = x[a];
+                        s_ld[a][tx] = 0.0;
                     }
-                    pcg_init(rng, P.init_nee, index);
-                    light = -1;
+                    pcg_init(rng, P.init_nee, s_idx[tx]);
+                    s_light[tx] = -1;
                     flight_done = true;  // fall through into "start next light"
-                    T = R(1);
                     phase = 2;
-                }
-            } else if (PAR) {
-                if (u2 * sm < sigma) {
+                } else {
                     flight_done = true;
                     collided = true;
                 }
-            } else {
-                // ratio tracking + Russian roulette below T < 0.1
-                T *= R(1) - sigma * inv_sm;
-                if (T < R(0.1)) {
-                    const R q = T * R(10);
-                    if (uniform(rng, R(0)) >= q) {
-                        T = R(0);
-                        flight_done = true;
-                    } else {
-                        T = R(0.1);
-                    }
+            }
+        } else {
+            if (phase != 1 && phase != 2) continue;
+            // ---- one tentative-collision step (shared by both flight kinds) ----
+            t -= par_step(rng, inv_sm);
+            ++nstep;
+            if (t > t1) {
+                if (phase == 1) {  // primary ray left the volume: background
+                    const size_t sb = 3 * (size_t)s_w[tx];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) slots[sb + c] = P.bg[c];
+                    phase = 0;
+                    continue;
                 }
+                flight_done = true;
+            } else {
+                // u2 is drawn before sigma(x) is evaluated: nothing else touches
+                // the stream in between, so the sequence is the reference's
+                const double u2sm = par_u2sm(rng, sm53);
+                if (par_certain_null(S, par_load(Fm, tx), t, s_tb[tx], u2sm)) continue;
+                s_u2[tx] = u2sm;  // park until the warp's next fetch round
+                phase |= 4;
+                continue;
             }
         }
         if (!flight_done) continue;
 
         // ---- a shadow flight ended (or the primary hit just happened) ----
+        int light = s_light[tx];
         if (light >= 0) {
-            if (PAR) {
-                if (!collided) ++passed;
-                if (++trial < P.nee_trials) {
-                    t = ts0;
-                    continue;
-                }
-                T = (R)passed / (R)P.nee_trials;
+            s_nshad[tx] += nstep - s_mark[tx];
+            const int passed = s_passed[tx] + (collided ? 0 : 1);
+            const int trial = s_trial[tx] + 1;
+            if (trial < P.nee_trials) {
+                s_passed[tx] = passed;
+                s_trial[tx] = trial;
+                s_mark[tx] = nstep;
+                t = s_tb[tx];
+                continue;
             }
-            nee(light, T);
+            nee(light, (double)passed / (double)P.nee_trials);
         }
         // start the next light's segment x -> P (volume.cpp:230-238)
         for (;;) {
             ++light;
             if (light >= S.n_lights) break;
-            R dv[3] = {(R)S.light_p[light][0] - o[0], (R)S.light_p[light][1] - o[1],
-                       (R)S.light_p[light][2] - o[2]};
-            const R len = rsqrt_len(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
-            bool trivially_lit = (len == R(0));
+            double o[3] = {s_o[0][tx], s_o[1][tx], s_o[2][tx]};
+            double dv[3] = {S.light_p[light][0] - o[0], S.light_p[light][1] - o[1], S.light_p[light][2] - o[2]};
+            const double len = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+            bool trivially_lit = (len == 0.0);
             if (!trivially_lit) {
+                double d[3];
 #pragma unroll
-                for (int a = 0; a < 3; ++a) d[a] = dv[a] / len;
-                R a0, a1;
-                trivially_lit = !aabb_unit<R>(o, d, R(0), len, a0, a1) || !(sm > R(0));
+                for (int a = 0; a < 3; ++a) {
+                    d[a] = dv[a] / len;
+                    s_d[a][tx] = d[a];
+                }
+                double a0, a1;
+                trivially_lit = !aabb_unit<double>(o, d, 0.0, len, a0, a1) || !(sm > 0.0);
                 if (!trivially_lit) {
                     t = a0;
-                    ts0 = a0;
                     t1 = a1;
-                    trial = 0;
-                    passed = 0;
-                    T = R(1);
+                    s_tb[tx] = a0;
+                    {
+                        ParFlight F;
+                        par_flight(S, o, d, a0, F);
+                        par_store(Fm, tx, F);
+                    }
+                    s_trial[tx] = 0;
+                    s_passed[tx] = 0;
+                    s_mark[tx] = nstep;
                     break;
                 }
             }
-            nee(light, R(1));
+            nee(light, 1.0);
         }
+        s_light[tx] = light;
         if (light < S.n_lights) continue;  // shadow flight started
 
         // ---- all lights done: w_d * L_d into the slot, hit record for the field
+        const uint32_t w = s_w[tx];
         const size_t sb = 3 * (size_t)w;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) slots[sb + c] = (Slot)P.w_d * s_ld[c][tx];
+        for (int c = 0; c < 3; ++c) slots[sb + c] = P.w_d * s_ld[c][tx];
         if (P.use_field) {
             const unsigned long long h = warp_fetch_add(&P.counters[1], 1u);
             HitRec rec;
-            rec.x[0] = (float)o[0];
-            rec.x[1] = (float)o[1];
-            rec.x[2] = (float)o[2];
+            rec.x[0] = (float)s_o[0][tx];
+            rec.x[1] = (float)s_o[1][tx];
+            rec.x[2] = (float)s_o[2][tx];
             const float wz = fminf(fmaxf((float)s_wo[2][tx], -1.0f), 1.0f);
             rec.wsph[0] = acosf(wz) * (float)(1.0 / kPi);
             rec.wsph[1] = (atan2f((float)s_wo[1][tx], (float)s_wo[0][tx]) + (float)kPi) * (float)(0.5 / kPi);
             rec.slot = w;
-            rec.sigma_s = (double)sig_s;
+            rec.sigma_s = s_sig[tx];
             P.hits[h] = rec;
             if (P.hit_dir) {
 #pragma unroll
-                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = (double)s_wo[a][tx];
+                for (int a = 0; a < 3; ++a) P.hit_dir[3 * h + a] = s_wo[a][tx];
             }
         } else {
             warp_fetch_add(&P.counters[1], 1u);
         }
         phase = 0;
     }
-    atomicAdd(&P.counters[2], (unsigned long long)nprim);
-    atomicAdd(&P.counters[3], (unsigned long long)nshad);
+    atomicAdd(&P.counters[2], (unsigned long long)(nstep - s_nshad[tx]));
+    atomicAdd(&P.counters[3], (unsigned long long)s_nshad[tx]);
+    atomicAdd(&P.counters[4], (unsigned long long)s_nfetch[tx]);
 }
 
 // ---------------------------------------------------------------------------
 // Batched parity entry points (one thread per ray).
 // ---------------------------------------------------------------------------
-template <bool PAR>
+// pf::delta_track (volume.cpp:204-225), binary64: hit, Interaction{position,
+// scalar, albedo}.
 __global__ void k_delta_track_batch(const DevScene S, BatchParams B) {
-    using R = typename Prec<PAR>::R;
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.n) return;
     Pcg rng;
     pcg_init(rng, B.initstate, B.idx[i]);
-    R o[3], d[3];
+    double o[3], d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        o[a] = (R)B.a3[3 * i + a];
-        d[a] = (R)B.b3[3 * i + a];
+        o[a] = B.a3[3 * i + a];
+        d[a] = B.b3[3 * i + a];
     }
-    R t0, t1;
+    double t0, t1;
     B.hit[i] = 0;
-    if (!aabb_unit<R>(o, d, (R)B.tmin[i], (R)B.tmax[i], t0, t1)) return;
-    const R sm = majorant(S, R(0));
-    if (sm <= R(0)) return;
-    const R inv = inv_majorant(S, R(0));
-    R t = t0;
+    if (!aabb_unit<double>(o, d, B.tmin[i], B.tmax[i], t0, t1)) return;
+    const double sm = S.sigma_max;
+    if (sm <= 0.0) return;
+    const double inv = S.inv_sigma_max, sm53 = sm * 0x1.0p-53;
+    ParFlight F;
+    par_flight(S, o, d, t0, F);
+    double t = t0;
     for (;;) {
-        t -= step_len(rng, inv);
+        t -= par_step(rng, inv);
         if (t > t1) return;
-        R x[3] = {o[0] + d[0] * t, o[1] + d[1] * t, o[2] + d[2] * t};
-        const R u2 = uniform(rng, R(0));
-        if (u2 * sm >= (R)cell_bound(S, x)) continue;  // certain null collision
-        const R s = sample(S, x);
-        const R sigma = density(S, R(0)) * tf_alpha(S, s);
-        if (u2 * sm < sigma) {
+        const double u2sm = par_u2sm(rng, sm53);
+        if (par_certain_null(S, F, t, t0, u2sm)) continue;
+        double x[3] = {o[0] + d[0] * t, o[1] + d[1] * t, o[2] + d[2] * t};
+        const double s = sample_d(S, x);
+        const double sigma = S.density_scale * tf_alpha_d(S, s);
+        if (u2sm < sigma) {
             B.hit[i] = 1;
             if (B.pos3)
-                for (int a = 0; a < 3; ++a) B.pos3[3 * i + a] = (double)x[a];
+                for (int a = 0; a < 3; ++a) B.pos3[3 * i + a] = x[a];
+            if (B.scalar) B.scalar[i] = s;
             if (B.rgba4) {
-                R c[4];
-                tf_rgba(S, s, c);
-                for (int a = 0; a < 4; ++a) B.rgba4[4 * i + a] = (double)c[a];
+                double c[4];
+                tf_rgba_d(S, s, c);
+                for (int a = 0; a < 4; ++a) B.rgba4[4 * i + a] = c[a];
             }
             return;
         }
     }
 }
 
-#ifdef PF_TU_PARITY
 // transmittance(medium, a, b, rng, n_trials), volume.cpp:227-256 (binary64).
 __global__ void k_transmittance_batch(const DevScene S, BatchParams B) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -381,18 +439,20 @@ __global__ void k_transmittance_batch(const DevScene S, BatchParams B) {
         return;
     }
     int passed = 0;
+    const double inv = S.inv_sigma_max, sm53 = S.sigma_max * 0x1.0p-53;
+    ParFlight F;
+    par_flight(S, a, dir, t0, F);
     for (int trial = 0; trial < B.n_trials; ++trial) {
         double t = t0;
         bool collided = false;
-        const double inv = 1.0 / S.sigma_max;
         for (;;) {
-            t -= log(1.0 - pcg_double(rng)) * inv;
+            t -= par_step(rng, inv);
             if (t > t1) break;
+            const double u2sm = par_u2sm(rng, sm53);
+            if (par_certain_null(S, F, t, t0, u2sm)) continue;
             double x[3] = {a[0] + dir[0] * t, a[1] + dir[1] * t, a[2] + dir[2] * t};
-            const double u2 = pcg_double(rng);
-            if (u2 * S.sigma_max >= cell_bound(S, x)) continue;  // certain null collision
-            const double sigma = S.density_scale * tf_alpha_d(S, sample_d(S, x));
-            if (u2 * S.sigma_max < sigma) {
+            const double sigma = S.density_scale * tf_alpha_d(S, sample_d(S, x));  // Medium::extinction
+            if (u2sm < sigma) {
                 collided = true;
                 break;
             }

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
     }
     atomicAdd(&P.counters[2], (unsigned long long)nprim);
     atomicAdd(&P.counters[3], (unsigned long long)nshad);
+    atomicAdd(&P.counters[4], (unsigned long long)(nprim + nshad));  // every tentative collision fetches
 }
 
 cudaError_t launch_render_trace_fast(const DevScene &S, const TraceParams &P, int grid, cudaStream_t st) {
@@ -222,6 +223,7 @@ __global__ void k_delta_track_batch_dda(const DevScene S, BatchParams B) {
             B.hit[i] = 1;
             if (B.pos3)
                 for (int a = 0; a < 3; ++a) B.pos3[3 * i + a] = (double)x[a];
+            if (B.scalar) B.scalar[i] = (double)s;
             if (B.rgba4) {
                 float c[4];
                 tf_rgba_f(S, s, c);

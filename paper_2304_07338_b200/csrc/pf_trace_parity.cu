@@ -8,14 +8,14 @@ namespace pfk {
 
 cudaError_t launch_render_trace_parity(const DevScene &S, const TraceParams &P, int grid,
                                        cudaStream_t st) {
-    k_render_trace<true><<<grid, PF_TRACE_THREADS, 0, st>>>(S, P);
+    k_render_trace_parity<<<grid, PF_TRACE_THREADS, 0, st>>>(S, P);
     return cudaGetLastError();
 }
 
 cudaError_t launch_delta_track_batch_parity(const DevScene &S, const BatchParams &B,
                                             cudaStream_t st) {
     const unsigned blocks = (unsigned)((B.n + 127) / 128);
-    k_delta_track_batch<true><<<blocks, 128, 0, st>>>(S, B);
+    k_delta_track_batch<<<blocks, 128, 0, st>>>(S, B);
     return cudaGetLastError();
 }
 
@@ -34,7 +34,7 @@ cudaError_t launch_rng_doubles(const BatchParams &B, cudaStream_t st) {
 int trace_grid_size_parity(int device) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_trace<true>, PF_TRACE_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_trace_parity, PF_TRACE_THREADS, 0);
     return sms * (per_sm > 0 ? per_sm : 1);
 }
 
