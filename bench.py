@@ -5,11 +5,16 @@
 
 One step = one full frame of render_neural (Alg. 2): 1920x1080, 8 spp, 256^3
 synthetic volume, one point light, paper-size photon field (16x8 hash grid,
-T = 2^19, 5x64 MLP), FAST mode (binary32 delta tracking + ratio-tracked NEE).
+T = 2^19, 5x64 MLP).  The headline is PARITY mode: the reference's own
+estimator (binary64 delta tracking against the global majorant, delta-trial
+NEE, the reference's RNG consumption; proj/src/volume.cpp:204-256), so
+value / e2e compare like-for-like with `--impl reference`, the unmodified
+reference CPU path on the host cores.  FAST mode (binary32, macro-cell DDA +
+ratio tracking, statistically equivalent) is reported under "fast".
 N > 1: image tiles are interleaved over the ranks (strong scaling of one
-frame) and gathered to rank 0 over NCCL.  Timing: W untimed warm-up frames,
-then K frames, each bracketed by CUDA events on the render stream with an L2
-flush (256 MiB write) between frames; barrier + synchronize around the timed
+frame) and gathered to rank 0.  Timing: W untimed warm-up frames, then K
+frames, each bracketed by CUDA events on the render stream with an L2 flush
+(256 MiB write) between frames; barrier + synchronize around the timed
 region; the max over ranks is reported.
 """
 from __future__ import annotations
@@ -128,21 +133,48 @@ class ClockSampler:
 
 # ------------------------------------------------------------ reference ----
 
-def reference_cpu_frame_sample(rows: int, workers: int, fc, params, vol, tf, lights, cam_spec):
-    """The reference CPU render path on `rows` rows of the frame, taken as 8
-    bands spread evenly over the image (the volume's coverage varies with y,
-    so a single central band would bias the per-frame extrapolation)."""
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def reference_inputs():
+    """Config-2 inputs for the reference CPU path WITHOUT the GPU library: the
+    paper field's parameters come from the oracle's restatement of
+    pf_field_init (same draw order, tests/test_host.py pins the equality)."""
+    from types import SimpleNamespace as NS
+
     from oracle import oracle as o
-    from paper_2304_07338_b200 import RenderConfig
-    sc = o.RefScene(vol, tf, 100.0)
-    rc = RenderConfig(spp=SPP, g=0.0, seed=SEED, mode="parity", use_field=True)
-    bands = min(8, rows)
-    per = max(1, rows // bands)
+    vol, tf, lights, cam = scene_inputs()
+    fc = NS(pos=NS(dims=3, levels=16, features=8, base_res=4, growth=2.0, log2_table=19),
+            dir=NS(dims=2, levels=16, features=8, base_res=4, growth=2.0, log2_table=19),
+            hidden_layers=5, width=64, psi=5.0)
+    params = o.field_init(fc, seed=SEED, embed_scale=1e-2, bias_scale=0.0)
+    rc = NS(spp=SPP, g=0.0, seed=SEED, w_d=1.0, w_i=1.0, background=(0.0, 0.0, 0.0), nee_trials=1,
+            use_field=True)
+    return vol, tf, lights, cam, fc, params, rc
+
+
+def reference_cpu_frame(sc, lights, fc, params, cam_spec, rc, workers: int) -> tuple[float, int]:
+    """One WHOLE frame of the reference CPU render path: pf::delta_track +
+    pf::transmittance (proj/src/volume.cpp:204-256, compiled unmodified in
+    oracle/_ref) driven by pf::parallel_chunks in chunks of 4096 samples
+    (proj/src/parallel.cpp:22-49) on `workers` host threads, with the SPEC-only
+    pieces (camera, NEE term, binary64 field forward, compose) from the C
+    restatement.  Returns (seconds, hits)."""
+    from oracle import oracle as o
     t0 = time.perf_counter()
-    for b in range(bands):
-        y0 = int((b + 0.5) * H_ / bands) - per // 2
-        o.ref_render_neural(sc, lights, fc, params, cam_spec, rc, rect=(0, y0, W_, y0 + per), workers=workers)
-    return time.perf_counter() - t0, bands * per
+    if isinstance(sc, o.RefScene):
+        _, st = o.ref_render_neural(sc, lights, fc, params, cam_spec, rc, workers=workers)
+    else:  # no oracle/_ref on this host: the single-threaded C restatement ("port")
+        _, st = o.render_neural(sc, lights, fc, params, cam_spec, rc)
+    return time.perf_counter() - t0, int(st["hits"])
 
 
 def cpu_baseline_kind():
@@ -151,41 +183,37 @@ def cpu_baseline_kind():
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU path timed on the host cores."""
+    """--impl reference: the reference's own CPU path timed on the host cores,
+    whole config-2 frames (median of --steps frames after --warmup frames)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from oracle import oracle as o
-    from paper_2304_07338_b200 import FieldConfig
     workers = os.cpu_count() or 1
-    if not o.ref_available():
-        kind = "port"
-    else:
-        kind = "reference"
-    vol, tf, lights, cam = scene_inputs()
-    fc = FieldConfig.paper()
-    params = fc.init_params(seed=SEED, embed_scale=1e-2, bias_scale=0.0)
-    # size the per-step row band to ~3 s of CPU work
-    rows = 8
-    t, rows = reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam)
-    rows = int(min(H_, max(8, rows * 3.0 / max(t, 1e-3))))
+    kind = "reference" if o.ref_available() else "port"
+    vol, tf, lights, cam, fc, params, rc = reference_inputs()
+    sc = o.RefScene(vol, tf, 100.0) if kind == "reference" else o.OracleScene(vol, tf, 100.0)
+    t_wall0 = time.perf_counter()
     for _ in range(args.warmup):
-        reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam)
-    res = [reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam) for _ in range(args.steps)]
-    rows = res[0][1]
-    sec_per_frame = float(np.mean([r[0] for r in res])) * H_ / rows
-    fps = 1.0 / sec_per_frame
-    sample = (f"{rows} of {H_} rows (8 evenly spread bands) x {W_} px x {SPP} spp per step (full per-sample program: "
-              f"pf::delta_track + pf::transmittance via pf::parallel_chunks, fp64 field forward); "
-              f"frame time extrapolated by rows")
+        reference_cpu_frame(sc, lights, fc, params, cam, rc, workers)
+    res = [reference_cpu_frame(sc, lights, fc, params, cam, rc, workers) for _ in range(args.steps)]
+    wall = time.perf_counter() - t_wall0
+    sec = float(np.median([r[0] for r in res]))
+    fps = 1.0 / sec
+    sample = (f"whole frames: {W_}x{H_} px x {SPP} spp = {W_ * H_ * SPP} samples per step, median of "
+              f"{args.steps} frames after {args.warmup} warm-up frames; pf::delta_track + pf::transmittance "
+              f"(unmodified volume.cpp) via pf::parallel_chunks(chunk 4096 samples) + binary64 field forward")
     line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_per_frame * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "config 2: 256^3 sphere_sinusoid, 1920x1080, 8 spp, scene A TF, "
-                                   "1 light, paper field", "cpu": "host cores"},
+            "config": {"workload": CFG["desc"] + ", 1 point light, paper photon field (random init)",
+                       "mode": "parity", "cpu": f"{cpu_model()}, {workers} threads"},
+            "frame": {"samples": W_ * H_ * SPP, "hits": res[0][1],
+                      "sec_min": float(np.min([r[0] for r in res])),
+                      "sec_max": float(np.max([r[0] for r in res])), "wall_s": wall},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": kind,
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -194,16 +222,53 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ ours ----
 
+def trace_kernel_name(mode: str) -> str:
+    return "k_render_trace_fast" if mode == "fast" else "k_render_trace_parity"
+
+
+def load_traffic():
+    tfile = ROOT / "profiles" / "traffic.json"
+    return json.loads(tfile.read_text()) if tfile.exists() else {}
+
+
+def roofline_for(mode: str, stats: list, peaks, peak_kind: str, traffic: dict) -> dict:
+    """HBM roofline of the dominant kernel (the tracer) per SURVEY 8(d): 32 B
+    (8 x f32 voxels) per voxel fetch actually issued (PARITY skips the fetch of
+    every certain-null collision; FAST fetches at every tentative collision of
+    its macro-cell DDA), over the tracer's CUDA-event time on the render stream.
+    The tracers are issue-bound, so ncu's issue / FP64 pipe / lane figures for
+    the same kernel (profiles/, cold cache) ride along."""
+    kname = trace_kernel_name(mode)
+    tr_ms = float(np.mean([s["ms_trace"] for s in stats]))
+    steps = float(np.mean([s["primary_steps"] + s["shadow_steps"] for s in stats]))
+    fetches = float(np.mean([s["voxel_fetches"] for s in stats]))
+    hbm = float(peaks["hbm_gbs"])
+    achieved = fetches * 32.0 / (tr_ms * 1e-3) / 1e9
+    k = traffic.get("kernels", {}).get(kname, {})
+    return {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": k.get("dram_bytes"),
+            "per_unit": f"32 B (8 x f32 voxels) per voxel fetch issued, {fetches:.4g} fetches per launch "
+                        f"({steps:.4g} tentative collisions)",
+            "peak_source": peak_kind,
+            "tentative_collisions_per_s": steps / (tr_ms * 1e-3),
+            "issue": {"sm_issue_active_pct": k.get("sm_issue_active_pct"),
+                      "fp64_pipe_pct": k.get("fp64_pipe_pct"),
+                      "lane_efficiency": k.get("lane_efficiency"),
+                      "source": traffic.get("source")}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
+    ap.add_argument("--mode", default="parity", choices=["fast", "parity"],
+                    help="headline mode (parity = the reference's binary64 estimator)")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-fast", action="store_true", help="skip the FAST-mode extra line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     select_config(args.config)
@@ -247,8 +312,12 @@ def main():
     params = fc.init_params(seed=SEED, embed_scale=1e-2, bias_scale=0.0)
     ctx.load_field(fc, params)
     cam = ctx.camera(cam_spec)
-    rc = RenderConfig(spp=SPP, g=0.0, seed=SEED, mode=args.mode, use_field=True, tile=(16, 16),
-                      shard_index=rank, shard_count=world)
+
+    def rconf(mode):
+        return RenderConfig(spp=SPP, g=0.0, seed=SEED, mode=mode, use_field=True, tile=(16, 16),
+                            shard_index=rank, shard_count=world)
+
+    rc = rconf(args.mode)
     frame = torch.zeros((H_, W_, 3), dtype=torch.float32, device="cuda")
     n_tiles_max = max(ctx.tiles_count(cam, rc, s) for s in range(world))
     per_shard = n_tiles_max * 16 * 16 * 3
@@ -279,10 +348,9 @@ def main():
             gather = "nccl"
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     ctx.set_timing(True)
-
     frame_no = [0]
 
-    def step(stats=True):
+    def step(rc_, stats=True):
         if CFG["dynamic"]:  # config 5: new TF + light every frame
             tf_i, li_i = dynamic_scene(frame_no[0], tf, lights)
             ctx.set_medium(tf_i, 100.0)
@@ -290,126 +358,146 @@ def main():
         frame_no[0] += 1
         if gather == "p2p":
             dist.all_reduce(sync)  # rank 0 is done with the previous frame
-        st = ctx.render_neural(cam, rc, out=frame, stats=stats)
+        st = ctx.render_neural(cam, rc_, out=frame, stats=stats)
         if gather == "p2p":
             dist.all_reduce(sync)  # every rank's tiles are in rank 0's frame
         elif gather == "nccl":
-            ctx.tiles_pack(cam, rc, frame, packed)
+            ctx.tiles_pack(cam, rc_, frame, packed)
             dist.all_gather_into_tensor(gathered, packed)
             if rank == 0:
-                ctx.tiles_unpack(cam, rc, gathered, per_shard, frame)
+                ctx.tiles_unpack(cam, rc_, gathered, per_shard, frame)
         return st[1] if stats else None
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    stats = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t_wall0 = time.perf_counter()
-        for i in range(args.steps):
-            flush.fill_(float(i))                     # L2 flush between timed frames (untimed)
-            ev[i][0].record()
-            stats.append(step())
-            ev[i][1].record()
+    def time_frames(rc_):
+        """W warm-up frames, then K frames each bracketed by CUDA events on the
+        render stream, L2 flushed (256 MiB write, untimed) before each."""
+        for _ in range(args.warmup):
+            step(rc_)
         torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        stats = []
         if world > 1:
             dist.barrier()
-        wall = time.perf_counter() - t_wall0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(np.sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    fps = 1000.0 / ms_per_step
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            t_wall0 = time.perf_counter()
+            for i in range(args.steps):
+                flush.fill_(float(i))
+                ev[i][0].record()
+                stats.append(step(rc_))
+                ev[i][1].record()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            wall = time.perf_counter() - t_wall0
+        total_ms = max_over_ranks(float(np.sum([a.elapsed_time(b) for a, b in ev])))
+        return total_ms / args.steps, stats, clk.summary(), wall
 
-    # per-kernel (this rank): trace kernel dominates; algorithmic bytes = 32 B / tentative step
-    tr_ms = float(np.mean([s["ms_trace"] for s in stats]))
-    fld_ms = float(np.mean([s["ms_field"] for s in stats]))
-    steps_tot = float(np.mean([s["primary_steps"] + s["shadow_steps"] for s in stats]))
-    hits = float(np.mean([s["hits"] for s in stats]))
-    samples = float(np.mean([s["samples"] for s in stats]))
-    peaks, peak_kind = load_peaks()
-    hbm = float(peaks["hbm_gbs"])
-    achieved = steps_tot * 32.0 / (tr_ms * 1e-3) / 1e9
-    traffic = sm_issue = None
-    tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():
-        tj = json.loads(tfile.read_text())
-        kname = "k_render_trace_fast" if args.mode == "fast" else "k_render_trace_parity"
-        traffic = tj.get(kname)
-        sm_issue = tj.get("sm_throughput_pct", {}).get(kname)
-
-    # ---- e2e: public API with host buffers (per-frame TF/light/camera in, frame out)
-    e2e = None
-    if rank == 0 or world > 1:
+    def time_e2e(rc_):
+        """The public API with HOST buffers: per-frame TF + lights in, the frame
+        out to pinned host memory, host<->device copies inside the timed region."""
         host_frame = torch.empty((H_, W_, 3), dtype=torch.float32, pin_memory=True)
         tf_h = torch.from_numpy(tf.copy()).pin_memory()
         li_h = torch.from_numpy(lights.copy()).pin_memory()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        e_times = []
         if world == 1:
-            # pipelined public API: frame i's device->host copy overlaps frame i+1's
-            # kernels (pf_render_neural_async); every frame is read back before the
-            # loop ends, inputs (TF, lights) uploaded every frame
+            # pipelined: frame i's device->host copy overlaps frame i+1's kernels
+            # (pf_render_neural_async); every frame is read back before the loop ends
             hosts = [host_frame, torch.empty_like(host_frame).pin_memory()]
-            for i in range(3):  # warm-up of the async path
-                ctx.render_neural_async(cam, rc, hosts[i % 2].numpy())
+            for i in range(3):
+                ctx.render_neural_async(cam, rc_, hosts[i % 2].numpy())
             ctx.synchronize()
             t0 = time.perf_counter()
             for i in range(args.steps):
-                ctx.set_medium(tf_h.numpy(), 100.0)       # per-frame TF (config 5 style)
+                ctx.set_medium(tf_h.numpy(), 100.0)
                 ctx.set_lights(li_h.numpy())
-                ctx.render_neural_async(cam, rc, hosts[i % 2].numpy())
+                ctx.render_neural_async(cam, rc_, hosts[i % 2].numpy())
                 if i > 0:
                     ctx.frame_wait(hosts[(i - 1) % 2].numpy())
             ctx.frame_wait(hosts[(args.steps - 1) % 2].numpy())
-            e_times = [(time.perf_counter() - t0) / args.steps]
+            e_ms = (time.perf_counter() - t0) / args.steps * 1e3
         else:
+            times = []
             for i in range(args.steps):
                 t0 = time.perf_counter()
                 ctx.set_medium(tf_h.numpy(), 100.0)
                 ctx.set_lights(li_h.numpy())
-                step(stats=False)
+                step(rc_, stats=False)
                 if rank == 0:
                     host_frame.copy_(frame, non_blocking=True)
                 torch.cuda.synchronize()
-                e_times.append(time.perf_counter() - t0)
-        e_ms = float(np.mean(e_times)) * 1e3
-        if world > 1:
-            t = torch.tensor([e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+                times.append(time.perf_counter() - t0)
+            e_ms = float(np.mean(times)) * 1e3
+        e_ms = max_over_ranks(e_ms)
         h2d = tf.nbytes + lights.nbytes + 104 + 128   # TF + lights + camera + render desc
-        e2e = {"value": 1000.0 / e_ms, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(H_ * W_ * 12) if rank == 0 else 0}
+        return {"value": 1000.0 / e_ms, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(H_ * W_ * 12) if rank == 0 else 0}
 
-    # ---- extras (rank 0): field-query throughput (part c) and KNN gather (config 3)
+    peaks, peak_kind = load_peaks()
+    traffic = load_traffic()
+
+    def frame_summary(stats, wall):
+        hits = float(np.mean([s["hits"] for s in stats]))
+        samples = float(np.mean([s["samples"] for s in stats]))
+        steps = float(np.mean([s["primary_steps"] + s["shadow_steps"] for s in stats]))
+        return {"samples": samples * world, "hits": hits, "hit_fraction": hits / max(samples, 1),
+                "steps_per_sample": steps / max(samples, 1),
+                "voxel_fetches": float(np.mean([s["voxel_fetches"] for s in stats])),
+                "ms_trace": float(np.mean([s["ms_trace"] for s in stats])),
+                "ms_field": float(np.mean([s["ms_field"] for s in stats])),
+                "ms_compose": float(np.mean([s["ms_compose"] for s in stats])), "wall_s": wall}
+
+    # ---- headline: the reference's estimator (PARITY, binary64) unless --mode fast
+    ms_per_step, stats, clocks, wall = time_frames(rc)
+    fps = 1000.0 / ms_per_step
+    samples = float(np.mean([s["samples"] for s in stats]))
+    e2e = time_e2e(rc)
+    launches = int(sum(s["kernel_launches"] for s in stats)) + (2 * args.steps if gather == "nccl" else 0)
+
+    # ---- FAST mode (binary32, macro-cell DDA + ratio-tracked NEE) as an extra
+    fast = None
+    if args.mode == "parity" and not args.no_fast:
+        rcf = rconf("fast")
+        f_ms, f_stats, f_clk, f_wall = time_frames(rcf)
+        fast = {"value": 1000.0 / f_ms, "unit": "frames/s", "ms_per_step": f_ms, "dtype": "f32",
+                "note": "binary32 delta tracking against macro-cell majorants + ratio-tracked shadow rays: "
+                        "a different, unbiased estimator (statistical parity with the reference, "
+                        "tests/test_gpu_c2.py); NOT the headline",
+                "mrays_per_s": samples * world / (f_ms * 1e-3) / 1e6,
+                "frame": frame_summary(f_stats, f_wall),
+                "roofline": roofline_for("fast", f_stats, peaks, peak_kind, traffic),
+                "e2e": time_e2e(rcf), "clocks": f_clk,
+                "gpu_launches": int(sum(s["kernel_launches"] for s in f_stats))}
+
+    # ---- extras (every rank runs its own query shard; rank 0 reports the aggregate)
     extras = {}
-    if not args.no_extras:  # every rank runs its own query shard; rank 0 reports the aggregate
+    if not args.no_extras:
         extras = bench_extras(ctx, fc, params, peaks, rank, world, cam=cam, rc=rc, frame=frame)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
+        try:  # the reference CPU path: 3 whole frames on the host cores, median
+            from oracle import oracle as o
             workers = os.cpu_count() or 1
-            rows = 8
-            t, rows = reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam_spec)
-            rows = int(min(H_, max(8, rows * 12.0 / max(t, 1e-3))))
-            t, rows = reference_cpu_frame_sample(rows, workers, fc, params, vol, tf, lights, cam_spec)
-            cpu = {"value": (rows / H_) / t, "unit": "frames/s", "cores": workers,
-                   "kind": cpu_baseline_kind(),
-                   "sample": f"{rows}/{H_} rows (8 evenly spread bands) of the same frame ({rows * W_ * SPP} samples), "
-                             f"{t:.1f} s; reference delta_track/transmittance + fp64 field"}
+            rvol, rtf, rlights, rcam, rfc, rparams, rrc = reference_inputs()
+            kind = cpu_baseline_kind()
+            sc = o.RefScene(rvol, rtf, 100.0) if kind == "reference" else o.OracleScene(rvol, rtf, 100.0)
+            ts = [reference_cpu_frame(sc, rlights, rfc, rparams, rcam, rrc, workers)[0] for _ in range(3)]
+            cpu = {"value": 1.0 / float(np.median(ts)), "unit": "frames/s", "cores": workers, "kind": kind,
+                   "cpu_model": cpu_model(),
+                   "sample": f"3 whole frames ({W_ * H_ * SPP} samples each), median {np.median(ts):.2f} s; "
+                             f"unmodified pf::delta_track/transmittance via parallel_chunks(4096) + "
+                             f"binary64 field"}
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -422,28 +510,21 @@ def main():
             "dtype": "f32" if args.mode == "fast" else "f64", "data": "synthetic",
             "config": {"workload": CFG["desc"] + ", 1 point light, paper photon field "
                                                  "(16x8 hash grid T=2^19, 5x64 MLP, random init)",
-                       "mode": args.mode, "tiles": "16x16 interleaved over ranks",
+                       "mode": args.mode,
+                       "estimator": ("reference: binary64 delta tracking with the global majorant, "
+                                     "delta-trial NEE, the reference's RNG consumption"
+                                     if args.mode == "parity" else "fast: binary32 macro-cell DDA + ratio tracking"),
+                       "tiles": "16x16 interleaved over ranks",
                        "l2": "flushed (256 MiB write) between timed frames",
                        "parallelism": f"tiles{world}", "gather": gather},
             "mrays_per_s": samples * world / (ms_per_step * 1e-3) / 1e6,
-            "frame": {"samples": samples * world, "hits": hits, "hit_fraction": hits / max(samples, 1),
-                      "steps_per_sample": steps_tot / max(samples, 1),
-                      "ms_trace": tr_ms, "ms_field": fld_ms, "wall_s": wall},
-            "roofline": {"kernel": "k_render_trace_fast" if args.mode == "fast" else "k_render_trace<parity>",
-                         "bound": "hbm",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic,
-                         "per_unit": "32 B (8 x f32 voxels) per tentative collision, "
-                                     f"{steps_tot:.3g} collisions per launch",
-                         "peak_source": peak_kind,
-                         # the macro-cell majorants remove ~97% of the reference's tentative
-                         # collisions, so the kernel is issue/latency-bound, not HBM-bound:
-                         # ncu's SM throughput (% of peak) for it, from profiles/ (cold cache)
-                         "sm_throughput_pct_ncu": sm_issue},
+            "frame": frame_summary(stats, wall),
+            "roofline": roofline_for(args.mode, stats, peaks, peak_kind, traffic),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) + (2 * args.steps if gather == "nccl" else 0),
-            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "fast": fast,
             **extras,
         }
         print(json.dumps(line), flush=True)

@@ -385,6 +385,7 @@ __global__ void k_delta_track_batch(const DevScene S, BatchParams B) {
     }
     double t0, t1;
     B.hit[i] = 0;
+    if (B.scalar) B.scalar[i] = 0.0;
     if (!aabb_unit<double>(o, d, B.tmin[i], B.tmax[i], t0, t1)) return;
     const double sm = S.sigma_max;
     if (sm <= 0.0) return;

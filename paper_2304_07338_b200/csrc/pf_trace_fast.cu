@@ -210,6 +210,7 @@ __global__ void k_delta_track_batch_dda(const DevScene S, BatchParams B) {
     }
     float t, t1;
     B.hit[i] = 0;
+    if (B.scalar) B.scalar[i] = 0.0;
     if (!aabb_unit<float>(o, d, (float)B.tmin[i], (float)B.tmax[i], t, t1) || !(S.sigma_max_f > 0.f) ||
         !occ_clip(S, o, d, t, t1))
         return;

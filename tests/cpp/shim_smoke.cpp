@@ -17,7 +17,10 @@ int main() {
         std::vector<pf::Ray> rays(4, pf::Ray{{0.5, 0.5, -1.0}, {0.0, 0.0, 1.0}, 0.0, pf::kInfinity});
         auto its = dev.delta_track(rays, 7, pf::Stream::CameraSample, {0, 1, 2, 3});
         int hits = 0;
-        for (auto &it : its) hits += it.has_value();
+        for (auto &it : its) {
+            hits += it.has_value();
+            if (it && it->scalar != 1.0) return 5;  // Interaction::scalar of the constant-1 grid
+        }
         dev.set_lights({pf::LightSource{{2.0, 2.5, -1.0}, {1.0, 1.0, 1.0}}});
         pf::TraceConfig tc;
         tc.n_total = 1000;

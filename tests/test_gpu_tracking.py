@@ -79,6 +79,25 @@ def test_delta_track_fp64_parity(scene):
     assert np.array_equal(c_g[both][same_bits], c_o[both][same_bits])
 
 
+def test_delta_track_interaction_scalar_matches_reference(scene, ref_oracle):
+    """Interaction{position, scalar, albedo} through the C ABI
+    (pf_delta_track_batch scalar1; volume.hpp:82-86, volume.cpp:223): bitwise
+    equal to the UNMODIFIED reference wherever the position is bitwise equal."""
+    ctx, osc = scene
+    n = 50000
+    o, d, tmin, tmax = _rays(n, 21)
+    idx = np.arange(n, dtype=np.uint64) * 5 + 3
+    h_g, p_g, s_g, c_g = ctx.delta_track_batch(o, d, tmin, tmax, 77, "camera", idx, fp64=True, with_scalar=True)
+    rsc = ref_oracle.RefScene(osc.vol, osc.tf, 100.0)
+    h_r, p_r, s_r, c_r = rsc.delta_track(o, d, tmin, tmax, 77, CAM, idx, with_scalar=True)
+    both = (h_g == 1) & (h_r == 1)
+    assert both.sum() > 1000 and np.count_nonzero(h_g != h_r) <= max(2, 1e-4 * n)
+    same = np.all(p_g[both].view(np.uint64) == p_r[both].view(np.uint64), axis=1)
+    assert np.array_equal(s_g[both][same].view(np.uint64), s_r[both][same].view(np.uint64))
+    assert np.array_equal(c_g[both][same].view(np.uint64), c_r[both][same].view(np.uint64))
+    assert np.all(s_g[h_g == 0] == 0.0)
+
+
 def test_delta_track_fast_statistics(scene):
     """FAST mode (binary32, macro-cell majorant DDA): unbiased free-flight
     sampling -> same hit probability and hit-depth distribution (KS)."""

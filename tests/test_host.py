@@ -158,3 +158,17 @@ def test_cpp_shim_against_reference_headers(pflib, tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert ("no gpu" in r.stdout) or ("gpu ok hits=4" in r.stdout)
+
+
+def test_oracle_field_init_matches_library(pflib, oracle):
+    """bench.py's reference arm builds its field parameters with the oracle's
+    restatement of pf_field_init (so it never loads the GPU library): both must
+    produce the same floats (SPEC.md:430 draw order)."""
+    from paper_2304_07338_b200 import FieldConfig
+    for fc in (FieldConfig.desk(), FieldConfig.paper()):
+        a = fc.init_params(seed=2024, embed_scale=1e-2, bias_scale=0.0)
+        b = oracle.field_init(fc, seed=2024, embed_scale=1e-2, bias_scale=0.0)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    fc = FieldConfig.desk()
+    a = fc.init_params(seed=3, embed_scale=0.5, bias_scale=0.1)
+    assert np.array_equal(a, oracle.field_init(fc, seed=3, embed_scale=0.5, bias_scale=0.1))
