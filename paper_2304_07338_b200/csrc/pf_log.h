@@ -40,6 +40,24 @@ static __device__ const pf_log_entry pf_log_tab_dev[1 << PF_LOG_BITS] = PF_LOG_T
 #endif
 static const pf_log_entry pf_log_tab_host[1 << PF_LOG_BITS] = PF_LOG_TABLE_INIT;
 
+// Polynomial / ln2 constants.  On the device they live in the constant bank so
+// the DFMAs take them as c[][] operands (64-bit immediates would cost two
+// uniform moves each, every step).
+#define PF_LOG_CONSTS                                                                                  \
+    {-0x1p-3, 0x1.2492492492492p-3, -0x1.5555555555555p-3, 0x1.999999999999ap-3, -0x1p-2,              \
+     0x1.5555555555555p-2, -0x1p-1, PF_LOG_LN2HI, PF_LOG_LN2LO}
+#if defined(__CUDACC__)
+static __constant__ double pf_log_c_dev[9] = PF_LOG_CONSTS;
+#endif
+static const double pf_log_c_host[9] = PF_LOG_CONSTS;
+#if defined(__CUDA_ARCH__) && !defined(PF_LOG_IMM)
+#define PF_LOG_C(i) pf_log_c_dev[i]
+#elif defined(__CUDA_ARCH__)
+#define PF_LOG_C(i) ((const double[9])PF_LOG_CONSTS)[i]
+#else
+#define PF_LOG_C(i) pf_log_c_host[i]
+#endif
+
 PF_LOG_HD uint64_t pf_log_bits(double x) {
 #if defined(__CUDA_ARCH__)
     return (uint64_t)__double_as_longlong(x);
@@ -111,21 +129,21 @@ PF_LOG_HD double pf_log(double y) {
     // kd = (double)k without a conversion instruction: 2^52 + (k + 1024) - (2^52 + 1024)
     const double kd = pf_log_sub(pf_log_dbl(0x4330000000000000ull | (uint32_t)(k + 1024)), 0x1.0000000000400p52);
     const double r = pf_log_fma(z, invc, -1.0);                    // exact
-    const double w = pf_log_fma(kd, PF_LOG_LN2HI, e.logc_hi);      // exact
+    const double w = pf_log_fma(kd, PF_LOG_C(7), e.logc_hi);       // exact
     // TwoSum(w, r)
     const double hi = pf_log_add(w, r);
     const double bb = pf_log_sub(hi, w);
     const double lo = pf_log_add(pf_log_sub(w, pf_log_sub(hi, bb)), pf_log_sub(r, bb));
     // log1p(r) - r = r^2 (c2 + c3 r + ... + c8 r^6)
     const double r2 = pf_log_mul(r, r);
-    double p = -0x1p-3;                                  // -1/8
-    p = pf_log_fma(p, r, 0x1.2492492492492p-3);          // 1/7
-    p = pf_log_fma(p, r, -0x1.5555555555555p-3);         // -1/6
-    p = pf_log_fma(p, r, 0x1.999999999999ap-3);          // 1/5
-    p = pf_log_fma(p, r, -0x1p-2);                       // -1/4
-    p = pf_log_fma(p, r, 0x1.5555555555555p-2);          // 1/3
-    p = pf_log_fma(p, r, -0x1p-1);                       // -1/2
-    double tail = pf_log_fma(kd, PF_LOG_LN2LO, logc_lo);
+    double p = PF_LOG_C(0);                 // -1/8
+    p = pf_log_fma(p, r, PF_LOG_C(1));      // 1/7
+    p = pf_log_fma(p, r, PF_LOG_C(2));      // -1/6
+    p = pf_log_fma(p, r, PF_LOG_C(3));      // 1/5
+    p = pf_log_fma(p, r, PF_LOG_C(4));      // -1/4
+    p = pf_log_fma(p, r, PF_LOG_C(5));      // 1/3
+    p = pf_log_fma(p, r, PF_LOG_C(6));      // -1/2
+    double tail = pf_log_fma(kd, PF_LOG_C(8), logc_lo);
     tail = pf_log_fma(r2, p, tail);
     return pf_log_add(hi, pf_log_add(lo, tail));
 }

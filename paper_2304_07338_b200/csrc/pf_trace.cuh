@@ -111,10 +111,13 @@ __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3],
 // keeps the step loop spill-free and short (~100 instructions vs ~280).
 // ---------------------------------------------------------------------------
 #ifndef PF_PAR_REFILL
-#define PF_PAR_REFILL 28  // waiting lanes that trigger a warp-wide refill
+#define PF_PAR_REFILL 4  // waiting lanes that trigger a refill from the warp queue
 #endif
 #ifndef PF_PAR_FETCH
 #define PF_PAR_FETCH 4  // lanes parked at a voxel fetch that trigger a fetch round
+#endif
+#ifndef PF_PAR_BURST
+#define PF_PAR_BURST 16  // tentative collisions per lane between warp-level checks
 #endif
 #ifndef PF_PAR_CTAS
 #define PF_PAR_CTAS 7  // resident CTAs per SM (register budget 65536 / (128 x 7) = 73)
@@ -164,62 +167,111 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
         for (int c = 0; c < 3; ++c) s_ld[c][tx] = Ld[c];
     };
 
-    // Lanes whose sample ended wait (phase 0) until PF_PAR_REFILL lanes of the
-    // warp are waiting (or none is tracking), then refill together: the
-    // ~300-instruction sample setup (work decode, camera ray, 6 binary64
-    // divisions, box clip) then runs once per group instead of once per lane
-    // with 1-2 lanes active (profiles/r02b_*: 25% of the kernel's instructions).
+    // Sample setup through a per-warp ready queue in shared memory: when a
+    // refill finds the queue empty, the WHOLE warp (converged, 32 lanes) sets up
+    // the next 32 work items at once -- work decode, camera ray, binary64
+    // divisions, box clip; rays that miss the box write their background slot
+    // here and are never queued -- so a waiting lane only copies one queue
+    // entry (~40 instructions) instead of running the ~300-instruction setup
+    // with a handful of lanes active.  Lanes wait (phase 0) until
+    // PF_PAR_REFILL of them are waiting or none is tracking.
+    __shared__ double q_d[3][PF_TRACE_THREADS], q_t0[PF_TRACE_THREADS], q_t1[PF_TRACE_THREADS];
+    __shared__ unsigned long long q_st[PF_TRACE_THREADS], q_idx[PF_TRACE_THREADS];
+    __shared__ uint32_t q_w[PF_TRACE_THREADS];
+    const int lane = tx & 31, wb = tx & ~31;  // this warp's 32 queue slots: [wb, wb + 32)
+    int qh = 0, qn = 0;                       // warp-uniform ring head / count
+    bool drained = false;                     // warp-uniform: the work counter ran out
+
+    auto take = [&](unsigned wmask) {
+        const int r = __popc(wmask & lanemask_lt());
+        if (phase == 0 && r < qn) {
+            const int q = wb + ((qh + r) & 31);
+            double o[3], d[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                o[a] = P.cam_o[a];
+                d[a] = q_d[a][q];
+                s_o[a][tx] = o[a];
+                s_d[a][tx] = d[a];
+                s_wo[a][tx] = -d[a];
+            }
+            const unsigned long long index = q_idx[q];
+            s_idx[tx] = index;
+            s_w[tx] = q_w[q];
+            rng.state = q_st[q];
+            rng.inc = (index << 1) | 1ull;
+            t = q_t0[q];
+            t1 = q_t1[q];
+            s_tb[tx] = t;
+            ParFlight F;
+            par_flight(S, o, d, t, F);
+            par_store(Fm, tx, F);
+            phase = 1;
+        }
+        const int got = min(__popc(wmask), qn);
+        qh = (qh + got) & 31;
+        qn -= got;
+    };
+    auto fill = [&]() {  // precondition: qn == 0, all 32 lanes converged
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&P.counters[0], 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base + 32ull >= (unsigned long long)P.n_work) drained = true;
+        bool ok = false;
+        const uint32_t w = (uint32_t)(base + (unsigned long long)lane);
+        int px = 0, py = 0;
+        uint64_t index = 0;
+        double d[3], t0 = 0, ta = 0;
+        Pcg r;
+        if (base + (unsigned long long)lane < (unsigned long long)P.n_work && decode_work(P, w, px, py, index)) {
+            pcg_init(r, P.init_cam, index);
+            const double u = pcg_double(r);
+            const double v = pcg_double(r);
+            // pinned camera (oracle or_camera_ray)
+            const double sx = (2.0 * ((double)px + u)) / (double)P.W - 1.0;
+            const double sy = 1.0 - (2.0 * ((double)py + v)) / (double)P.H;
+            double o[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                o[a] = P.cam_o[a];
+                d[a] = (P.cam_f[a] + P.cam_r[a] * sx) + P.cam_u[a] * sy;
+            }
+            const double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) d[a] = d[a] / len;
+            if (aabb_unit<double>(o, d, 0.0, rinf(0.0), t0, ta) && sm > 0.0) {
+                ok = true;
+            } else {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = P.bg[c];
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const int q = wb + ((qh + qn + __popc(m & lanemask_lt())) & 31);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) q_d[a][q] = d[a];
+            q_t0[q] = t0;
+            q_t1[q] = ta;
+            q_st[q] = r.state;
+            q_idx[q] = index;
+            q_w[q] = w;
+        }
+        qn += __popc(m);
+    };
+
     for (;;) {
         const unsigned waiting = __ballot_sync(0xffffffffu, phase == 0);
         const unsigned tracking = __ballot_sync(0xffffffffu, phase == 1 || phase == 2);
         const unsigned parked = __ballot_sync(0xffffffffu, (phase & 4) != 0);
         if (waiting && (tracking == 0 || __popc(waiting) >= PF_PAR_REFILL)) {
-            while (phase == 0) {
-                const uint32_t w = (uint32_t)warp_fetch_add(&P.counters[0], 1u);
-                if (w >= P.n_work) {
-                    phase = 3;  // queue drained
-                    break;
-                }
-                int px, py;
-                uint64_t index;
-                if (!decode_work(P, w, px, py, index)) continue;
-                s_w[tx] = w;
-                s_idx[tx] = index;
-                pcg_init(rng, P.init_cam, index);
-                const double u = pcg_double(rng);
-                const double v = pcg_double(rng);
-                // pinned camera (oracle or_camera_ray)
-                const double sx = (2.0 * ((double)px + u)) / (double)P.W - 1.0;
-                const double sy = 1.0 - (2.0 * ((double)py + v)) / (double)P.H;
-                double o[3], d[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    o[a] = P.cam_o[a];
-                    d[a] = (P.cam_f[a] + P.cam_r[a] * sx) + P.cam_u[a] * sy;
-                }
-                const double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    d[a] = d[a] / len;
-                    s_wo[a][tx] = -d[a];
-                    s_o[a][tx] = o[a];
-                    s_d[a][tx] = d[a];
-                }
-                double t0;
-                if (!aabb_unit<double>(o, d, 0.0, rinf(0.0), t0, t1) || !(sm > 0.0)) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) slots[3 * (size_t)w + c] = P.bg[c];
-                    continue;
-                }
-                t = t0;
-                s_tb[tx] = t0;
-                {
-                    ParFlight F;
-                    par_flight(S, o, d, t0, F);
-                    par_store(Fm, tx, F);
-                }
-                phase = 1;
+            take(waiting);
+            const unsigned still = __ballot_sync(0xffffffffu, phase == 0);
+            if (still && qn == 0 && !drained) {
+                fill();
+                take(still);
             }
+            if (drained && qn == 0 && phase == 0) phase = 3;  // no work left for this lane
             continue;  // re-evaluate the warp's state
         }
         if (tracking == 0 && parked == 0) break;  // every lane drained
@@ -260,27 +312,42 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
             }
         } else {
             if (phase != 1 && phase != 2) continue;
-            // ---- one tentative-collision step (shared by both flight kinds) ----
-            t -= par_step(rng, inv_sm);
-            ++nstep;
-            if (t > t1) {
-                if (phase == 1) {  // primary ray left the volume: background
-                    const size_t sb = 3 * (size_t)s_w[tx];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) slots[sb + c] = P.bg[c];
-                    phase = 0;
-                    continue;
+            // ---- a burst of up to PF_PAR_BURST tentative-collision steps ----
+            // (shared by both flight kinds; the warp-level bookkeeping above runs
+            // once per burst, a lane leaves the burst at its first event)
+            const ParFlight F = par_load(Fm, tx);
+            const double tb = s_tb[tx];
+            int ev = 0;  // 0 none, 1 left the segment, 2 parked at a voxel fetch
+#pragma unroll 1
+            for (int k = 0; k < PF_PAR_BURST; ++k) {
+                t -= par_step(rng, inv_sm);
+                ++nstep;
+                if (t > t1) {
+                    ev = 1;
+                    break;
                 }
-                flight_done = true;
-            } else {
                 // u2 is drawn before sigma(x) is evaluated: nothing else touches
                 // the stream in between, so the sequence is the reference's
                 const double u2sm = par_u2sm(rng, sm53);
-                if (par_certain_null(S, par_load(Fm, tx), t, s_tb[tx], u2sm)) continue;
-                s_u2[tx] = u2sm;  // park until the warp's next fetch round
+                if (!par_certain_null(S, F, t, tb, u2sm)) {
+                    s_u2[tx] = u2sm;  // park until the warp's next fetch round
+                    ev = 2;
+                    break;
+                }
+            }
+            if (ev == 0) continue;
+            if (ev == 2) {
                 phase |= 4;
                 continue;
             }
+            if (phase == 1) {  // primary ray left the volume: background
+                const size_t sb = 3 * (size_t)s_w[tx];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) slots[sb + c] = P.bg[c];
+                phase = 0;
+                continue;
+            }
+            flight_done = true;
         }
         if (!flight_done) continue;
 
