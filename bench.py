@@ -363,7 +363,10 @@ def main():
             dist.all_reduce(sync)  # every rank's tiles are in rank 0's frame
         elif gather == "nccl":
             ctx.tiles_pack(cam, rc_, frame, packed)
-            dist.all_gather_into_tensor(gathered, packed)
+            if dist.get_backend() == "nccl":
+                dist.all_gather_into_tensor(gathered, packed)
+            else:  # gloo (the one-GPU smoke test of this path): list all_gather
+                dist.all_gather(list(gathered.view(world, -1).unbind(0)), packed)
             if rank == 0:
                 ctx.tiles_unpack(cam, rc_, gathered, per_shard, frame)
         return st[1] if stats else None
@@ -502,6 +505,12 @@ def main():
             cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
 
+    dump = os.environ.get("PF_BENCH_DUMP")  # tests: rank 0 saves the last headline frame
+    if dump:
+        step(rc, stats=False)
+        torch.cuda.synchronize()
+        if rank == 0:
+            np.save(dump, frame.cpu().numpy())
     if rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,

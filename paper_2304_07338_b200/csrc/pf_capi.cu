@@ -1156,6 +1156,8 @@ int pf_trace_photons(pf_ctx *c, const pf_trace_desc *d, size_t *n_photons, uint6
             if (d->phase_set[h] == d->phase_set[g]) return set_err(PF_ERR_INVALID, "TraceConfig: phase values must be distinct");
     }
     if (d->max_bounces < 1) return set_err(PF_ERR_INVALID, "TraceConfig: max_bounces must be positive");
+    if (d->max_bounces > 65536)  // deposit ordinals travel in 16 bits (pf_photon.cu)
+        return set_err(PF_ERR_INVALID, "TraceConfig: max_bounces must be <= 65536");
     if (d->rr_start_bounce < 0) return set_err(PF_ERR_INVALID, "TraceConfig: rr_start_bounce must be >= 0");
     if (!(d->rr_min_survival > 0.0 && d->rr_min_survival <= d->rr_max_survival && d->rr_max_survival <= 1.0))
         return set_err(PF_ERR_INVALID, "TraceConfig: need 0 < rr_min_survival <= rr_max_survival <= 1");

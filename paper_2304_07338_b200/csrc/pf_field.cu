@@ -354,6 +354,11 @@ const char *field_validate(const FieldDesc &d) {
     }
     if ((d.pos.levels * d.pos.features) % 8 != 0 || (d.dir.levels * d.dir.features) % 8 != 0)
         return "field: levels*features must be a multiple of 8 for each grid";
+    // the direction tables start right after the position tables and are read
+    // with F_dir-wide vector loads (fp16 encode, fp32 Adam): keep them aligned
+    if (field_grid_param_count(d.pos) % (size_t)d.dir.features != 0)
+        return "field: position table parameters must be a multiple of the direction feature count "
+               "(16-byte aligned direction tables)";
     if (!(d.psi > 0.0)) return "field: psi must be positive";
     return nullptr;
 }

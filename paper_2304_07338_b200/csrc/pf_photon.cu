@@ -113,8 +113,11 @@ __global__ void __launch_bounds__(128, 7) k_trace_photons(const DevScene S, cons
                         r.pow[k] = (float)(s_scale[k][tx] * s_thr[k][tx]);
                     }
                     r.g_index = (uint8_t)gi;
-                    r.pad[0] = (uint8_t)dep;
-                    r.pad[1] = r.pad[2] = 0;
+                    // deposit ordinal (16 bits in pad[0..1]; max_bounces <= 65536
+                    // is enforced by pf_trace_photons)
+                    r.pad[0] = (uint8_t)(dep & 0xff);
+                    r.pad[1] = (uint8_t)(dep >> 8);
+                    r.pad[2] = 0;
                     P.rec[slot] = r;
                     P.rec_photon[slot] = (uint32_t)i;
                 }
@@ -147,8 +150,8 @@ __global__ void k_photon_scatter(const PhotonOut *rec, const uint32_t *rec_photo
     const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     PhotonOut p = rec[r];
-    const uint64_t dst = (uint64_t)offs[rec_photon[r]] + p.pad[0];
-    p.pad[0] = 0;
+    const uint64_t dst = (uint64_t)offs[rec_photon[r]] + ((uint32_t)p.pad[0] | ((uint32_t)p.pad[1] << 8));
+    p.pad[0] = p.pad[1] = 0;
     out[dst] = p;
 }
 

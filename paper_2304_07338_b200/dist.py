@@ -139,7 +139,8 @@ def train_step_dp(ctx, x3, wsph2, g, targets3, n_global: int, step: int, total: 
             t = t.cpu()
         dist.all_reduce(t, op=op, group=group)
         buf.copy_(t.to(buf.dtype))
-    lt = torch.tensor([loss], dtype=torch.float64)
+    # NCCL reduces device tensors only; gloo host tensors
+    lt = torch.tensor([loss], dtype=torch.float64, device="cpu" if host else gtab.device)
     dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=group)
     if gtab.is_cuda:
         torch.cuda.synchronize()

@@ -3,9 +3,9 @@
 Tolerance (north_star: "field predictions within a stated relative-error
 tolerance"): the device stores tables/weights/activations in fp16 with fp32
 accumulation; over a random wide-init field we require
-  |L'_gpu - L'_oracle| <= 2e-2 + 2e-2 * |L'_oracle|  per channel (log space),
-  median abs error <= 4e-3,
-and decoded radiance relative error <= psi*ln(10)*that (checked on 99.9%).
+  |L'_gpu - L'_oracle| <= 4e-3  per channel (log space; measured max 1.5e-3
+  desk / 1.9e-3 paper, so ~2x headroom),  median abs error <= 5e-4 (measured 2.5e-4),
+and decoded radiance relative error <= psi*ln(10)*4e-3 (checked on 99.9%).
 """
 import numpy as np
 import pytest
@@ -25,9 +25,16 @@ def _queries(n, seed):
     return x, w, g
 
 
-@pytest.mark.parametrize("cfg_name", ["desk", "paper"])
+def _cfg(name):
+    from paper_2304_07338_b200 import HashGrid
+    if name == "mixed":  # 8-wide position entries, 4-wide direction entries
+        return FieldConfig(HashGrid(3, 8, 8, 4, 2.0, 15), HashGrid(2, 8, 4, 4, 2.0, 15))
+    return getattr(FieldConfig, name)()
+
+
+@pytest.mark.parametrize("cfg_name", ["desk", "paper", "mixed"])
 def test_field_forward_matches_oracle(ctx, oracle, cfg_name):
-    fc = getattr(FieldConfig, cfg_name)()
+    fc = _cfg(cfg_name)
     assert fc.param_count() == oracle.field_param_count(fc)
     params = fc.init_params(seed=1, embed_scale=1.0, bias_scale=0.1)
     ctx.load_field(fc, params)
@@ -38,12 +45,12 @@ def test_field_forward_matches_oracle(ctx, oracle, cfg_name):
                                g.astype(np.float64))
     err = np.abs(out - ref)
     print(cfg_name, "max", err.max(), "median", np.median(err), "ref scale", np.abs(ref).mean())
-    assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref))
-    assert np.median(err) <= 4e-3
+    assert err.max() <= 4e-3
+    assert np.median(err) <= 5e-4
     dec = ctx.field_query(x, w, g, decoded=True)
     rdec = 10.0 ** (-np.clip(ref, 0, 1) * fc.psi)
     rel = np.abs(dec - rdec) / rdec
-    assert np.quantile(rel, 0.999) < fc.psi * np.log(10) * 2.5e-2
+    assert np.quantile(rel, 0.999) < fc.psi * np.log(10) * 4e-3
 
 
 def test_field_batch_equals_per_item(ctx):

@@ -73,6 +73,12 @@ def test_field_validation_messages(pflib):
     bad = FieldConfig(HashGrid(3, 3, 2), HashGrid(2, 3, 2))    # 12 features: not a multiple of 8
     with pytest.raises(ValueError, match="multiple of 8"):
         bad.param_count()
+    # desk position grid (169,607 entries x 4) ahead of 8-wide direction entries:
+    # the direction tables would start 8-byte aligned under 16-byte vector loads
+    bad = FieldConfig(HashGrid(3, 8, 4), HashGrid(2, 8, 8))
+    with pytest.raises(ValueError, match="aligned"):
+        bad.param_count()
+    assert FieldConfig(HashGrid(3, 8, 8), HashGrid(2, 8, 4)).param_count() > 0   # mixed, aligned
 
 
 def test_volume_and_tf_roundtrip(tmp_path):
