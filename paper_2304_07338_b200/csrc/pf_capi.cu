@@ -236,6 +236,7 @@ struct pf_ctx {
         S.density_scale = density_scale;
         S.sigma_max = sigma_max;
         S.inv_sigma_max = sigma_max > 0.0 ? 1.0 / sigma_max : 0.0;
+        S.sm53 = sigma_max * 0x1.0p-53;
         S.density_scale_f = (float)density_scale;
         S.sigma_max_f = (float)sigma_max;
         S.inv_sigma_max_f = sigma_max > 0.0 ? (float)(1.0 / sigma_max) : 0.f;

@@ -37,6 +37,7 @@ struct DevScene {
     int n_tf;
     int n_lights;
     double density_scale, sigma_max, inv_sigma_max;
+    double sm53;  // sigma_max * 2^-53 (exact): next_double() * sigma_max in one multiply
     float density_scale_f, sigma_max_f, inv_sigma_max_f;
     double tf_s[PF_MAX_TF];
     double tf_c[PF_MAX_TF][4];

@@ -105,11 +105,15 @@ PF_LOG_HD double pf_log_mul(double a, double b) {
 #endif
 }
 
-PF_LOG_HD double pf_log(double y) {
+// log(y * 2^escale) for y a positive normal double and y * 2^escale normal: the same
+// operations as pf_log(y * 2^escale), with escale folded into the exponent k only, so
+// the result is bit-identical (z, r and the table index do not depend on escale).
+PF_LOG_HD double pf_log_scaled(double y, int escale) {
     const uint64_t ix = pf_log_bits(y);
     const uint32_t hx = (uint32_t)(ix >> 32);
     const uint32_t tmp = hx - PF_LOG_OFF_HI;
-    const int k = (int32_t)tmp >> 20;
+    const int kraw = (int32_t)tmp >> 20;
+    const int k = kraw + escale;
     const uint32_t i = (tmp >> (20 - PF_LOG_BITS)) & ((1u << PF_LOG_BITS) - 1u);
 #if defined(__CUDA_ARCH__)
     pf_log_entry e;  // one 16-byte load
@@ -123,7 +127,7 @@ PF_LOG_HD double pf_log(double y) {
 #else
     const pf_log_entry e = pf_log_tab_host[i];
 #endif
-    const double z = pf_log_dbl(((uint64_t)(hx - ((uint32_t)k << 20)) << 32) | (ix & 0xffffffffull));
+    const double z = pf_log_dbl(((uint64_t)(hx - ((uint32_t)kraw << 20)) << 32) | (ix & 0xffffffffull));
     const double invc = pf_log_dbl((uint64_t)e.invc_hi << 32);
     const double logc_lo = pf_log_dbl((uint64_t)e.logc_lo_hi << 32);
     // kd = (double)k without a conversion instruction: 2^52 + (k + 1024) - (2^52 + 1024)
@@ -147,5 +151,7 @@ PF_LOG_HD double pf_log(double y) {
     tail = pf_log_fma(r2, p, tail);
     return pf_log_add(hi, pf_log_add(lo, tail));
 }
+
+PF_LOG_HD double pf_log(double y) { return pf_log_scaled(y, 0); }
 
 }  // namespace pfk

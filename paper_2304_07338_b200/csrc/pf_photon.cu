@@ -49,7 +49,7 @@ __device__ __forceinline__ bool track(const DevScene &S, const double o[3], cons
     double t0, t1;
     if (!aabb_unit<double>(o, d, 0.0, rinf(0.0), t0, t1)) return false;
     if (S.sigma_max <= 0.0) return false;
-    const double inv = S.inv_sigma_max, sm53 = S.sigma_max * 0x1.0p-53;
+    const double inv = S.inv_sigma_max, sm53 = S.sm53;
     ParFlight F;
     par_flight(S, o, d, t0, F);
     double t = t0;

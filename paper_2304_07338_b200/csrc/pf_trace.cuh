@@ -57,7 +57,7 @@ __device__ __forceinline__ bool decode_work(const TraceParams &P, uint32_t w, in
 
 // ----- precision-dispatched primitives ------------------------------------
 __device__ __forceinline__ double step_len(Pcg &r, double inv) {
-    return pf_log(1.0 - pcg_double(r)) * inv;  // volume.cpp:217 / 247 (pf_log.h)
+    return par_step(r, inv);  // volume.cpp:217 / 247 (pf_parstep.cuh)
 }
 __device__ __forceinline__ float step_len(Pcg &r, float inv) {
     return __logf(pcg_one_minus_u_f(r)) * inv;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
     double *slots = reinterpret_cast<double *>(P.slots);
     const double inv_sm = S.inv_sigma_max;
     const double sm = S.sigma_max;
-    const double sm53 = S.sigma_max * 0x1.0p-53;
+    const double sm53 = S.sm53;
     const double ds = S.density_scale;
     const double g = P.g;
 
@@ -456,7 +456,7 @@ __global__ void k_delta_track_batch(const DevScene S, BatchParams B) {
     if (!aabb_unit<double>(o, d, B.tmin[i], B.tmax[i], t0, t1)) return;
     const double sm = S.sigma_max;
     if (sm <= 0.0) return;
-    const double inv = S.inv_sigma_max, sm53 = sm * 0x1.0p-53;
+    const double inv = S.inv_sigma_max, sm53 = S.sm53;
     ParFlight F;
     par_flight(S, o, d, t0, F);
     double t = t0;
@@ -507,7 +507,7 @@ __global__ void k_transmittance_batch(const DevScene S, BatchParams B) {
         return;
     }
     int passed = 0;
-    const double inv = S.inv_sigma_max, sm53 = S.sigma_max * 0x1.0p-53;
+    const double inv = S.inv_sigma_max, sm53 = S.sm53;
     ParFlight F;
     par_flight(S, a, dir, t0, F);
     for (int trial = 0; trial < B.n_trials; ++trial) {
