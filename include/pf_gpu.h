@@ -357,9 +357,15 @@ typedef struct {
     const double *seg_radius;  /* strictly increasing radii */
     double psi;                /* Eq. 7 precision */
     uint64_t seed;
+    uint64_t start_step;       /* resume: first step to run (a checkpoint's next step); 0 = fresh run */
+    uint64_t stop_step;        /* run steps [start_step, stop_step) (checkpoint in chunks); 0 = total_steps */
 } pf_train_desc;
 /* ms_knn_steps / ms_step_steps (total_steps doubles each, may be NULL): the
- * per-step split for the training log. */
+ * per-step split for the training log.  Only steps
+ * [start_step, stop_step) run -- radius schedule, query streams, lr and Adam
+ * bias correction use the absolute step and total_steps, so a run split into
+ * chunks (with a checkpoint between them) is bit-identical to one call -- and
+ * only those entries of loss_history / ms_*_steps are written. */
 int pf_train(pf_ctx *ctx, const pf_train_desc *desc, double *loss_history, double *ms_knn,
              double *ms_step, double *ms_knn_steps, double *ms_step_steps);
 /* Optimizer state (checkpoint / resume): master parameters and

@@ -4,7 +4,7 @@ The product is the sm_100a C-ABI library libpfgpu.so (include/pf_gpu.h);
 this package is its Python host mirror of the reference's pf:: API.
 """
 from .api import (AdamConfig, Context, FieldConfig, HashGrid, PathTraceConfig, RenderConfig,  # noqa: F401
-                  TraceConfig, TraceResult, TrainConfig, TrainResult, load_checkpoint, lr_at,
+                  TraceConfig, TraceResult, TrainConfig, TrainResult, checkpoint_training_state, load_checkpoint, lr_at,
                   save_checkpoint, schedule_radius)
 from .scene import (CameraSpec, default_lights, load_photon_map, load_volume,  # noqa: F401
                     save_photon_map, save_volume, synth_photons, synth_volume, tf_scene_a,

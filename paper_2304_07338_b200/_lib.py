@@ -87,7 +87,8 @@ class AdamDesc(C.Structure):
 
 class TrainDesc(C.Structure):
     _fields_ = [("total_steps", C.c_uint64), ("batch", C.c_size_t), ("K", C.c_int), ("n_segments", C.c_int),
-                ("seg_end", _P_), ("seg_radius", _P_), ("psi", C.c_double), ("seed", C.c_uint64)]
+                ("seg_end", _P_), ("seg_radius", _P_), ("psi", C.c_double), ("seed", C.c_uint64),
+                ("start_step", C.c_uint64), ("stop_step", C.c_uint64)]
 
 
 _SIG = {

@@ -170,6 +170,7 @@ class TrainResult:
     step_ms_steps: np.ndarray = None
     radius: np.ndarray = None
     lr: np.ndarray = None
+    first_step: int = 0  # absolute step of entry 0 (a resumed run starts at its checkpoint)
 
     def write_log(self, path) -> None:
         """Training log, one line per step: step, loss, radius, lr,
@@ -178,7 +179,7 @@ class TrainResult:
         with open(path, "w") as f:
             f.write("step,loss,radius,lr,knn_time_ms\n")
             for i, l in enumerate(self.loss_history):
-                f.write(f"{i},{l:.17g},{self.radius[i]:.17g},{self.lr[i]:.17g},{cum[i]:.6f}\n")
+                f.write(f"{self.first_step + i},{l:.17g},{self.radius[i]:.17g},{self.lr[i]:.17g},{cum[i]:.6f}\n")
 
 
 def lr_at(step: int, total: int, adam: "AdamConfig | None" = None) -> float:
@@ -191,32 +192,40 @@ def lr_at(step: int, total: int, adam: "AdamConfig | None" = None) -> float:
 _CKPT_MAGIC = b"PFFC"
 
 
-def save_checkpoint(path, cfg: "FieldConfig", phase_set, step: int, params, m, v) -> None:
-    """Field checkpoint: header (configs, psi, G, next step), then the
-    flat parameter vector and both Adam moments, little-endian binary64."""
+def save_checkpoint(path, cfg: "FieldConfig", phase_set, step: int, params, m, v,
+                    adam: "AdamConfig | None" = None, total_steps: int = 0) -> None:
+    """Field checkpoint: header (configs, psi, G, next step, the
+    Adam hyperparameters and the run's total_steps -- everything train() needs
+    to continue at `step`), then the flat parameter vector and both Adam
+    moments, little-endian binary64.  Version 2 (version 1 had no Adam block)."""
     import struct
     gs = np.asarray(phase_set, np.float64)
+    a = adam or AdamConfig()
     with open(path, "wb") as f:
-        f.write(_CKPT_MAGIC + struct.pack("<I", 1))
+        f.write(_CKPT_MAGIC + struct.pack("<I", 2))
         for hg in (cfg.pos, cfg.dir):
             f.write(struct.pack("<iiiidi", hg.dims, hg.levels, hg.features, hg.base_res, float(hg.growth),
                                 hg.log2_table))
         f.write(struct.pack("<iid", cfg.hidden_layers, cfg.width, float(cfg.psi)))
         f.write(struct.pack("<I", len(gs)) + gs.astype("<f8").tobytes())
+        f.write(struct.pack(_CKPT_ADAM, a.lr, a.beta1, a.beta2, a.eps, a.decay, a.decay_start, a.eps_rel,
+                            int(a.decay_interval), int(total_steps)))
         f.write(struct.pack("<QQ", int(step), len(params)))
         for arr in (params, m, v):
             f.write(np.asarray(arr, np.float64).astype("<f8").tobytes())
 
 
-def load_checkpoint(path):
-    """-> (FieldConfig, phase_set, next step, params, m, v) (binary64 arrays)."""
+_CKPT_ADAM = "<7diQ"
+
+
+def _parse_checkpoint(path):
     import struct
     with open(path, "rb") as f:
         buf = f.read()
     if buf[:4] != _CKPT_MAGIC:
         raise ValueError("field checkpoint: bad magic")
     (ver,) = struct.unpack_from("<I", buf, 4)
-    if ver != 1:
+    if ver not in (1, 2):
         raise ValueError(f"field checkpoint: unsupported version {ver}")
     o = 8
     grids = []
@@ -230,12 +239,30 @@ def load_checkpoint(path):
     o += 4
     gs = np.frombuffer(buf, "<f8", ng, o).copy()
     o += 8 * ng
+    adam, total = None, 0
+    if ver == 2:
+        lr, b1, b2, eps, dec, dstart, erel, dint, total = struct.unpack_from(_CKPT_ADAM, buf, o)
+        o += struct.calcsize(_CKPT_ADAM)
+        adam = AdamConfig(lr, b1, b2, eps, dec, dstart, dint, erel)
     step, n = struct.unpack_from("<QQ", buf, o)
     o += 16
     arrs = [np.frombuffer(buf, "<f8", n, o + 8 * n * k).copy() for k in range(3)]
     if o + 24 * n != len(buf):
         raise ValueError("field checkpoint: truncated or oversized")
-    return FieldConfig(pos=grids[0], dir=grids[1], hidden_layers=hl, width=wd, psi=psi), list(gs), step, *arrs
+    cfg = FieldConfig(pos=grids[0], dir=grids[1], hidden_layers=hl, width=wd, psi=psi)
+    return cfg, list(gs), step, arrs, adam, total
+
+
+def load_checkpoint(path):
+    """-> (FieldConfig, phase_set, next step, params, m, v) (binary64 arrays)."""
+    cfg, gs, step, arrs, _, _ = _parse_checkpoint(path)
+    return cfg, gs, step, *arrs
+
+
+def checkpoint_training_state(path):
+    """-> (AdamConfig or None for a version-1 file, total_steps (0 = unknown))."""
+    _, _, _, _, adam, total = _parse_checkpoint(path)
+    return adam, total
 
 
 @dataclass
@@ -446,20 +473,27 @@ class Context:
     def train_commit(self) -> None:
         check(lib().pf_train_commit(self._h))
 
-    def train(self, cfg: TrainConfig) -> TrainResult:
-        """train(field, map, cfg) on the resident photon map."""
+    def train(self, cfg: TrainConfig, start_step: int = 0, stop_step: int | None = None) -> TrainResult:
+        """train(field, map, cfg) on the resident photon map,
+        steps [start_step, stop_step or total).  start_step > 0 continues a run
+        restored by train_load (its next step): schedule radius, query streams,
+        lr and Adam bias correction use the absolute step, so train(stop=k) ->
+        train_save -> train_load -> train(start=k) reproduces the uninterrupted
+        run bit for bit.  The result covers the steps run."""
         ends = np.ascontiguousarray(cfg.schedule_ends, np.float64)
         radii = np.ascontiguousarray(cfg.schedule_radii, np.float64)
         d = _lib.TrainDesc(int(cfg.total_steps), int(cfg.batch_size), int(cfg.K), len(ends), ends.ctypes.data,
-                           radii.ctypes.data, float(cfg.psi), int(cfg.seed))
-        n = int(cfg.total_steps)
+                           radii.ctypes.data, float(cfg.psi), int(cfg.seed), int(start_step),
+                           int(stop_step or 0))
+        n, s0 = int(cfg.total_steps), int(start_step)
+        s1 = int(stop_step) if stop_step else n
         hist, ka, kb = np.zeros(n), np.zeros(n), np.zeros(n)
         a, b = C.c_double(), C.c_double()
         check(lib().pf_train(self._h, C.byref(d), hist.ctypes.data, C.byref(a), C.byref(b), ka.ctypes.data,
                              kb.ctypes.data))
-        radius = np.array([schedule_radius(cfg.schedule_ends, cfg.schedule_radii, s, n) for s in range(n)])
-        lrs = np.array([lr_at(s, n, getattr(self, "adam_config", None)) for s in range(n)])
-        return TrainResult(hist, a.value, b.value, ka, kb, radius, lrs)
+        radius = np.array([schedule_radius(cfg.schedule_ends, cfg.schedule_radii, s, n) for s in range(s0, s1)])
+        lrs = np.array([lr_at(s, n, getattr(self, "adam_config", None)) for s in range(s0, s1)])
+        return TrainResult(hist[s0:s1], a.value, b.value, ka[s0:s1], kb[s0:s1], radius, lrs, first_step=s0)
 
     def train_state(self):
         """(params, m, v) of the optimizer, binary32."""
@@ -468,14 +502,18 @@ class Context:
         check(lib().pf_train_state_get(self._h, *[o.ctypes.data for o in out], n_params))
         return tuple(out)
 
-    def train_save(self, path, phase_set, next_step: int) -> None:
+    def train_save(self, path, phase_set, next_step: int, total_steps: int = 0) -> None:
         p, m, v = self.train_state()
-        save_checkpoint(path, self.field_config, phase_set, next_step, p, m, v)
+        save_checkpoint(path, self.field_config, phase_set, next_step, p, m, v,
+                        adam=getattr(self, "adam_config", None), total_steps=total_steps)
 
     def train_load(self, path, adam: "AdamConfig | None" = None):
         """Restore a checkpoint bit-exactly (binary32 state stored as binary64);
-        returns (FieldConfig, phase_set, next step)."""
-        cfg, gs, step, p, m, v = load_checkpoint(path)
+        returns (FieldConfig, phase_set, next step).  The Adam hyperparameters
+        come from the checkpoint unless `adam` overrides them."""
+        cfg, gs, step, (p, m, v), ck_adam, _ = _parse_checkpoint(path)
+        if adam is None:
+            adam = ck_adam
         p32, m32, v32 = (np.ascontiguousarray(x, np.float32) for x in (p, m, v))
         if not (np.array_equal(p32.astype(np.float64), p) and np.array_equal(m32.astype(np.float64), m)
                 and np.array_equal(v32.astype(np.float64), v)):

@@ -1621,6 +1621,9 @@ int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms
     if (d->K < 1 || d->K > 1024) return set_err(PF_ERR_INVALID, "KnnQuery: K must be in [1, 1024]");
     if (!(d->psi > 0.0)) return set_err(PF_ERR_INVALID, "EncodingConfig: psi must be positive");
     if (!c->has_knn) return set_err(PF_ERR_INVALID, "pf_train: call pf_knn_build first");
+    const uint64_t stop = d->stop_step ? d->stop_step : d->total_steps;
+    if (stop > d->total_steps || d->start_step > stop)
+        return set_err(PF_ERR_INVALID, "pf_train: need start_step <= stop_step <= total_steps");
     PF_CUDA(cudaSetDevice(c->device));
     TrainState &S = c->train;
     const size_t B = d->batch;
@@ -1636,7 +1639,7 @@ int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms
     for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
     double knn_ms = 0.0, step_ms = 0.0;
     const uint64_t init = stream_initstate(d->seed, PF_STREAM_TRAIN);
-    for (uint64_t step = 0; step < d->total_steps; ++step) {
+    for (uint64_t step = d->start_step; step < stop; ++step) {
         // schedule_radius
         const double progress = (double)(step + 1) / (double)d->total_steps;
         double r = d->seg_radius[d->n_segments - 1];
@@ -1670,8 +1673,9 @@ int pf_train(pf_ctx *c, const pf_train_desc *d, double *loss_history, double *ms
         if (ms_step_steps) ms_step_steps[step] = b;
     }
     for (auto &e : ev) cudaEventDestroy(e);
-    if (loss_history)
-        PF_CUDA(cudaMemcpyAsync(loss_history, S.loss_dev.p, d->total_steps * 8, cudaMemcpyDefault, c->stream));
+    if (loss_history && stop > d->start_step)
+        PF_CUDA(cudaMemcpyAsync(loss_history + d->start_step, (const double *)S.loss_dev.p + d->start_step,
+                                (stop - d->start_step) * 8, cudaMemcpyDefault, c->stream));
     PF_CUDA(cudaStreamSynchronize(c->stream));
     if (ms_knn) *ms_knn = knn_ms;
     if (ms_step) *ms_step = step_ms;

@@ -193,3 +193,38 @@ def test_training_log(ctx, traced_map, tmp_path):
     assert np.array_equal(cols[:, 0], np.arange(40))
     assert set(cols[:, 2]) == {0.1, 0.2} and np.all(np.diff(cols[:, 4]) >= 0)
     assert abs(res.knn_ms - res.knn_ms_steps.sum()) < 1e-6 * max(1.0, res.knn_ms)
+
+
+def test_train_resume_through_checkpoint(ctx, traced_map, tmp_path):
+    """SPEC.md:439 through the public loop: train(stop=k) -> train_save ->
+    train_load (Adam hyperparameters from the checkpoint) -> train(start=k) is
+    bit-identical to one uninterrupted train() -- same parameters, moments
+    and per-step losses (the radius schedule, query streams, lr and bias
+    correction all continue at the absolute step)."""
+    from paper_2304_07338_b200 import checkpoint_training_state
+    fc = FieldConfig.desk()
+    adam = AdamConfig(lr=2e-3, decay_start=0.5, decay_interval=3)
+    tc = TrainConfig(total_steps=12, batch_size=1024, K=32, schedule_ends=(0.5, 1.0), schedule_radii=(0.1, 0.2),
+                     seed=5)
+    p0 = fc.init_params(seed=3, embed_scale=1e-2, bias_scale=0.0)
+    ctx.train_init(fc, p0, adam)
+    full = ctx.train(tc)
+    a = ctx.train_state()
+    ctx.train_init(fc, p0, adam)
+    first = ctx.train(tc, stop_step=5)
+    assert first.first_step == 0 and len(first.loss_history) == 5
+    ck = tmp_path / "chunk.pffc"
+    ctx.train_save(ck, ctx.phase_set, 5, tc.total_steps)
+    assert checkpoint_training_state(ck) == (adam, 12)
+    ctx.train_init(fc, fc.init_params(seed=99, embed_scale=0.5))  # clobber the optimizer state
+    cfg, gs, nxt = ctx.train_load(ck)
+    assert cfg == fc and nxt == 5 and ctx.adam_config == adam
+    rest = ctx.train(tc, start_step=nxt)
+    assert rest.first_step == 5 and len(rest.loss_history) == 7
+    b = ctx.train_state()
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    assert np.array_equal(np.concatenate([first.loss_history, rest.loss_history]), full.loss_history)
+    log = tmp_path / "rest.csv"
+    rest.write_log(log)
+    assert log.read_text().splitlines()[1].startswith("5,")

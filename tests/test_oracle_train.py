@@ -96,14 +96,16 @@ def test_sparse_adam_only_touches_visited_entries(oracle):
 
 
 def test_checkpoint_file_roundtrip(tmp_path):
-    from paper_2304_07338_b200 import load_checkpoint, lr_at, save_checkpoint
+    from paper_2304_07338_b200 import AdamConfig, checkpoint_training_state, load_checkpoint, lr_at, save_checkpoint
     fc = FieldConfig.desk()
     p = fc.init_params(seed=2, embed_scale=0.2)
     m, v = p * 0.5, np.abs(p) * 1e-3
     f = tmp_path / "x.pffc"
-    save_checkpoint(f, fc, [-0.75, 0.0, 0.75], 12, p, m, v)
+    adam = AdamConfig(lr=1e-3, beta2=0.999, decay_interval=7, eps_rel=0.02)
+    save_checkpoint(f, fc, [-0.75, 0.0, 0.75], 12, p, m, v, adam=adam, total_steps=40)
     cfg, gs, step, p2, m2, v2 = load_checkpoint(f)
     assert cfg == fc and gs == [-0.75, 0.0, 0.75] and step == 12
+    assert checkpoint_training_state(f) == (adam, 40)
     for a, b in ((p, p2), (m, m2), (v, v2)):
         assert np.array_equal(a.astype(np.float64), b)
     f.write_bytes(f.read_bytes()[:-8])
