@@ -624,11 +624,12 @@ def bench_extras(ctx, fc, params, peaks, rank=0, world=1, cam=None, rc=None, fra
     import bench_train
     out["field_training"] = bench_train.run(ctx, steps=10)
     out["field_training"]["ranks"] = world
-    # config 3: KNN radiance estimate (k = 64) over a 4M-photon 3-phase map,
-    # 2^20 device-resident queries per batch, CUDA-event timed
+    # config 3: KNN radiance estimate (k = 64) over 4M-photon 3-phase maps
+    # (uniform, clustered, traced) x r_max in {inf, 0.05, 0.25}, 2^20
+    # device-resident Stream::Train queries per batch, CUDA-event timed
     sys.path.insert(0, str(ROOT / "tools"))
     import bench_knn
-    k = bench_knn.run(ctx)
+    k = bench_knn.run(ctx, hbm_gbs=float(peaks["hbm_gbs"]))
     k["queries_per_s"] = _sum_over_ranks(k["queries_per_s"], world)
     k["algorithmic_GBps"] = _sum_over_ranks(k["algorithmic_GBps"], world)
     k["ranks"], k["scaling"] = world, "weak"

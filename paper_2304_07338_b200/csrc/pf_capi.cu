@@ -612,7 +612,7 @@ static constexpr size_t kFieldRowCap = (size_t)1 << 22;
 
 // encode + MLP over n_max items (count on device for renders), in row batches
 static int run_field(pf_ctx *c, FieldParams P, size_t n_max, uint32_t *launches = nullptr) {
-    const size_t row_bytes = (size_t)P.nch * 128u;  // 16 KB per chunk per 128 rows
+    const size_t row_bytes = (size_t)P.nch * (size_t)field_chunk_cols() * 2u;  // fp16 columns per row
     const size_t cap = std::min(n_max, std::max(kFieldRowCap, kFieldStageBytes / row_bytes));
     PF_CUDA(c->f_feat.ensure(field_feat_bytes(c->fhost, cap)));
     P.feat = (uint8_t *)c->f_feat.p;
@@ -645,7 +645,7 @@ static FieldParams field_params(pf_ctx *c) {
     for (size_t i = 0; i < h.levels.size(); ++i) P.lv[i] = h.levels[i];
     P.tables = (const __half *)c->f_tables.p;
     P.img = c->f_img.p;
-    P.nch = (h.K0 + 63) / 64;
+    P.nch = (h.K0 + field_chunk_cols() - 1) / field_chunk_cols();
     P.row_cap = kFieldRowCap;
     return P;
 }

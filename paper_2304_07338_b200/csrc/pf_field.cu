@@ -32,14 +32,24 @@
 namespace pfk {
 
 
+// Feature tiles are staged in chunks of PF_FIELD_CW columns (128 rows x CW
+// fp16 = CW * 256 bytes, one bulk-TMA copy each): the MLP keeps
+// a_bytes / chunk_bytes of them in flight per warpgroup while layer 0's MMAs
+// consume the previous ones.
+#ifndef PF_FIELD_CW
+#define PF_FIELD_CW 32
+#endif
+static_assert(PF_FIELD_CW == 16 || PF_FIELD_CW == 32 || PF_FIELD_CW == 64, "chunk width 16, 32 or 64 columns");
+constexpr uint32_t kFieldChunkBytes = PF_FIELD_CW * 256u;
+
 // Byte offset of element (row, k) in the feature-tile buffer: tile-major,
-// then 64-column chunks of 16 KB, each a canonical K-major UMMA tile.
+// then CW-column chunks, each a canonical K-major UMMA tile.
 __device__ __forceinline__ size_t feat_off(const FieldParams &P, size_t row, int k) {
     const size_t tile = row >> 7;
-    const int r = (int)(row & 127), chunk = k >> 6, kk = k & 63;
-    const int kw = min(64, P.K0 - 64 * chunk);
-    return (tile * (size_t)P.nch + (size_t)chunk) * 16384u + (size_t)((r >> 3) * kw * 16 + (kk >> 3) * 128 +
-                                                                     (r & 7) * 16 + (kk & 7) * 2);
+    const int r = (int)(row & 127), chunk = k / PF_FIELD_CW, kk = k % PF_FIELD_CW;
+    const int kw = min(PF_FIELD_CW, P.K0 - PF_FIELD_CW * chunk);
+    return (tile * (size_t)P.nch + (size_t)chunk) * kFieldChunkBytes +
+           (size_t)((r >> 3) * kw * 16 + (kk >> 3) * 128 + (r & 7) * 16 + (kk & 7) * 2);
 }
 
 template <int F>
@@ -122,10 +132,11 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
 
 // K4: the MLP on tcgen05.  Persistent CTA per SM with the whole MLP image in
 // shared memory; each warpgroup owns a 128-row tile pipeline:
-//   layer 0: chunk j of the feature tile arrives by ONE 1-D bulk TMA copy
-//            (double-buffered, mbarrier complete_tx) and is consumed by
-//            kw/16 tcgen05.mma (M=128, N=64, K=16) into a 64-column TMEM
-//            accumulator while chunk j+1 is in flight;
+//   layer 0: the tile's feature chunks (PF_FIELD_CW columns each) stream in
+//            by 1-D bulk TMA through NS = a_bytes / chunk-bytes slots
+//            (mbarrier complete_tx), so NS chunk loads are in flight while the
+//            kw/16 tcgen05.mma (M=128, N=64, K=16) of the oldest accumulate
+//            into the warpgroup's 64-column TMEM accumulator;
 //   layers 1..H: tcgen05.ld -> bias + ReLU -> fp16 -> st.shared into the A
 //            tile -> next layer's MMA (N=16 for the 3-wide output layer);
 //   epilogue: Eq. 8 decode, compose term into the sample's slot.
@@ -133,17 +144,18 @@ __global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *img = smem;
     uint8_t *abase = smem + P.img_bytes;
-    // barriers: [0] weights; per warpgroup w: 1+5w: full0, full1, empty0, empty1, done
-    // a_bytes per warpgroup: 32 KB = two chunk buffers (layer-0 double
-    // buffering), 16 KB = one (8 warpgroups per SM, layer-0 TMA latency hidden
-    // by the other warpgroups instead)
-    const int nb = P.a_bytes >= 32768u ? 2 : 1;
+    // barriers: [0] weights; per warpgroup w at 1 + (2 NS + 1) w: full[NS], empty[NS], done.
+    // The warpgroup's a_bytes of shared memory hold NS layer-0 chunk slots
+    // (filled by bulk TMA while the MMAs of earlier chunks run) and, from
+    // layer 1 on, the 16 KB activation tile.
+    const int NS = min(8, (int)(P.a_bytes / kFieldChunkBytes));
+    const int NB = 2 * NS + 1;
     uint64_t *bars = reinterpret_cast<uint64_t *>(abase + (size_t)P.n_wg * P.a_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + 5 * P.n_wg);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 1 + NB * P.n_wg);
 
     const int tid = threadIdx.x, wg = tid >> 7, r = tid & 127, warp = tid >> 5;
     if (tid == 0) {
-        for (int i = 0; i <= 5 * P.n_wg; ++i) mbar_init(smem_u32(&bars[i]), 1);
+        for (int i = 0; i <= NB * P.n_wg; ++i) mbar_init(smem_u32(&bars[i]), 1);
         mbar_fence_init();
     }
     if (warp == 0) tmem_alloc(smem_u32(tmem_slot), P.tmem_cols);
@@ -160,52 +172,50 @@ __global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
     const size_t n_all = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
     const size_t n_items = n_all > P.row0 ? min(n_all - P.row0, P.row_cap) : 0;
     const size_t n_tiles = (n_items + 127) / 128;
-    const uint32_t buf_s[2] = {smem_u32(abase + (size_t)wg * P.a_bytes),
-                               smem_u32(abase + (size_t)wg * P.a_bytes + (nb == 2 ? 16384u : 0u))};
+    const uint32_t abuf = smem_u32(abase + (size_t)wg * P.a_bytes);  // slot b at abuf + b * chunk bytes
     const uint32_t img_s = smem_u32(img);
     const uint32_t tmem_wg = tmem_base + (uint32_t)(wg * 64);
     const uint32_t tmem_rows = tmem_wg + ((uint32_t)(32 * (warp & 3)) << 16);
-    uint64_t *wb = bars + 1 + 5 * wg;
-    const uint32_t full[2] = {smem_u32(&wb[0]), smem_u32(&wb[1])};
-    const uint32_t empty[2] = {smem_u32(&wb[2]), smem_u32(&wb[3])};
-    const uint32_t done = smem_u32(&wb[4]);
-    uint32_t ph_full[2] = {0u, 0u}, ph_empty[2] = {0u, 0u}, ph_done = 0u;
-    bool empty_pending[2] = {false, false};
+    uint64_t *wb = bars + 1 + NB * wg;
+    const uint32_t full0 = smem_u32(&wb[0]), empty0 = smem_u32(&wb[NS]), done = smem_u32(&wb[2 * NS]);
+    uint32_t full_par = 0u, empty_par = 0u, pending = 0u, ph_done = 0u;  // per-slot phase bits
     const float *bias = reinterpret_cast<const float *>(img + P.off_bias);
     const uint32_t sbo_w0 = (uint32_t)P.K0 * 16u;
 
     for (size_t tile = (size_t)blockIdx.x * P.n_wg + wg; tile < n_tiles; tile += (size_t)gridDim.x * P.n_wg) {
-        const uint8_t *tsrc = P.feat + tile * (size_t)P.nch * 16384u;
+        const uint8_t *tsrc = P.feat + tile * (size_t)P.nch * kFieldChunkBytes;
         // ---- layer 0: TMA-fed chunks (only thread r == 0 drives the pipeline)
         if (r == 0) {
             auto load = [&](int j) {
-                const int b = j % nb;
-                if (empty_pending[b]) {
-                    mbar_wait(empty[b], ph_empty[b]);
-                    ph_empty[b] ^= 1u;
-                    empty_pending[b] = false;
+                const int b = j % NS;
+                if (pending & (1u << b)) {  // the slot's previous chunk is still being read by its MMAs
+                    mbar_wait(empty0 + 8u * b, (empty_par >> b) & 1u);
+                    empty_par ^= 1u << b;
+                    pending &= ~(1u << b);
                 }
-                const uint32_t bytes = (uint32_t)min(64, P.K0 - 64 * j) * 256u;  // 128 rows x kw x 2 B
-                mbar_expect_tx(full[b], bytes);
-                bulk_g2s(buf_s[b], tsrc + (size_t)j * 16384u, bytes, full[b]);
+                const uint32_t bytes = (uint32_t)min(PF_FIELD_CW, P.K0 - PF_FIELD_CW * j) * 256u;  // 128 rows x kw x 2 B
+                mbar_expect_tx(full0 + 8u * b, bytes);
+                bulk_g2s(abuf + (uint32_t)b * kFieldChunkBytes, tsrc + (size_t)j * kFieldChunkBytes, bytes,
+                         full0 + 8u * b);
             };
-            load(0);
+            for (int j = 0; j < NS && j < P.nch; ++j) load(j);
             for (int j = 0; j < P.nch; ++j) {
-                const int b = j % nb;
-                if (nb == 2 && j + 1 < P.nch) load(j + 1);  // prefetch into the other buffer
-                mbar_wait(full[b], ph_full[b]);
-                ph_full[b] ^= 1u;
+                const int b = j % NS;
+                mbar_wait(full0 + 8u * b, (full_par >> b) & 1u);
+                full_par ^= 1u << b;
                 tc_fence_after();
-                const int kw = min(64, P.K0 - 64 * j);
+                const int kw = min(PF_FIELD_CW, P.K0 - PF_FIELD_CW * j);
                 const uint32_t sbo = (uint32_t)kw * 16u, idesc = umma_idesc_f16(128, 64);
+                const uint32_t a0 = abuf + (uint32_t)b * kFieldChunkBytes;
+                const uint32_t b0 = img_s + P.off_w[0] + (uint32_t)(j * (PF_FIELD_CW / 8)) * 128u;
                 for (int s = 0; s < kw / 16; ++s) {
-                    const uint64_t ad = umma_sdesc(buf_s[b] + 256u * s, 128u, sbo);
-                    const uint64_t bd = umma_sdesc(img_s + P.off_w[0] + (uint32_t)(j * 8) * 128u + 256u * s, 128u, sbo_w0);
+                    const uint64_t ad = umma_sdesc(a0 + 256u * s, 128u, sbo);
+                    const uint64_t bd = umma_sdesc(b0 + 256u * s, 128u, sbo_w0);
                     umma_f16(tmem_wg, ad, bd, idesc, (j > 0 || s > 0) ? 1u : 0u);
                 }
-                umma_commit(empty[b]);
-                empty_pending[b] = true;
-                if (nb == 1 && j + 1 < P.nch) load(j + 1);  // waits for this chunk's MMAs
+                umma_commit(empty0 + 8u * b);
+                pending |= 1u << b;
+                if (j + NS < P.nch) load(j + NS);  // waits for this slot's MMAs, the other slots stay in flight
             }
             umma_commit(done);
         }
@@ -214,20 +224,19 @@ __global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
         named_bar_sync(1 + wg, 128);
         ph_done ^= 1u;
         tc_fence_after();
-        if (r == 0) {  // keep the per-buffer parities in step (both are complete by now)
-            for (int b = 0; b < 2; ++b)
-                if (empty_pending[b]) {
-                    mbar_wait(empty[b], ph_empty[b]);
-                    ph_empty[b] ^= 1u;
-                    empty_pending[b] = false;
+        if (r == 0) {  // keep the per-slot parities in step (every MMA is complete by now)
+            for (int b = 0; b < NS; ++b)
+                if (pending & (1u << b)) {
+                    mbar_wait(empty0 + 8u * b, (empty_par >> b) & 1u);
+                    empty_par ^= 1u << b;
                 }
+            pending = 0u;
         }
 
         // ---- hidden layers (epilogue of layer L-1 feeds the MMA of layer L)
         for (int L = 1; L <= P.hidden_layers; ++L) {
-            const int b = (L & 1) % nb;
             const float *bl = bias + (L - 1) * 64;
-            const uint32_t pa = buf_s[b] + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u;  // K=64: SBO 1024
+            const uint32_t pa = abuf + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u;  // K=64: SBO 1024
             // two halves of 32 columns: both 16-column loads of a half in flight, one wait
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(1024, 1) k_field_mlp(const FieldParams P) {
             named_bar_sync(1 + wg, 128);
             if (r == 0) {
                 tc_fence_after();
-                issue_layer(buf_s[b], img_s + P.off_w[L], 64, L < P.hidden_layers ? 64 : 16, tmem_wg);
+                issue_layer(abuf, img_s + P.off_w[L], 64, L < P.hidden_layers ? 64 : 16, tmem_wg);
                 umma_commit(done);
             }
             if ((r >> 5) == 0) mbar_wait(done, ph_done);
@@ -434,7 +443,7 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
 int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_bytes, int device) {
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    const size_t fixed = h.image.size() + 512;
+    const size_t fixed = h.image.size() + 2048;  // + mbarriers (<= 1 + 17 x 8) and the TMEM slot
     // preferred: 8 warpgroups x one 16 KB tile (8 tiles in flight per SM, TMEM
     // 8 x 64 columns); else up to 4 warpgroups x two 16 KB chunk buffers.
     // PF_MLP_WG=4 forces the double-buffered 4-warpgroup layout (A/B).
@@ -456,9 +465,11 @@ int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_b
     return n_wg > 0 ? 0 : 1;
 }
 
+int field_chunk_cols() { return PF_FIELD_CW; }
+
 size_t field_feat_bytes(const FieldHost &h, size_t n_items) {
-    const size_t nch = (size_t)((h.K0 + 63) / 64);
-    return ((n_items + 127) / 128) * nch * 16384u;
+    const size_t nch = (size_t)((h.K0 + PF_FIELD_CW - 1) / PF_FIELD_CW);
+    return ((n_items + 127) / 128) * nch * kFieldChunkBytes;
 }
 
 template <int FP, int FD>

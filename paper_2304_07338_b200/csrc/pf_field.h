@@ -80,5 +80,6 @@ int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_b
 cudaError_t launch_field(const FieldParams &P, int fp, int fd, int grid, size_t smem,
                          cudaStream_t st);
 size_t field_feat_bytes(const FieldHost &h, size_t n_items);
+int field_chunk_cols();  // feature-tile chunk width in columns (PF_FIELD_CW)
 
 }  // namespace pfk

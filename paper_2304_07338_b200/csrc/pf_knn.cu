@@ -455,6 +455,70 @@ __device__ __forceinline__ void sort_buf(uint64_t *buf, int n, unsigned lane) {
     __syncwarp();
 }
 
+// Ball-radius search: attempts before a query goes to the exact fallback.
+constexpr int kKnnAttempts = 24;
+
+// Distance from q to the phase's grid box (+ the binning slack): a lower bound
+// on every photon distance of the phase.
+__device__ __forceinline__ double knn_box_dist(const KnnGrid &Gp, const float q[3]) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double b0 = Gp.lo[a] - Gp.eps, b1 = Gp.lo[a] + (double)Gp.R[a] * Gp.h[a] + Gp.eps;
+        const double d = (double)q[a] < b0 ? b0 - (double)q[a] : ((double)q[a] > b1 ? (double)q[a] - b1 : 0.0);
+        d2 += d * d;
+    }
+    return sqrt(d2);
+}
+
+// Radius of the ball around q that contains the probe's cell cube (cells
+// qc -+ ring, clamped to the grid): when the cube held >= K photons, no ball
+// search ever needs to grow beyond it.
+__device__ __forceinline__ double knn_cube_reach(const KnnGrid &Gp, const float q[3], const int qc[3], int ring) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int c0 = max(qc[a] - ring, 0), c1 = min(qc[a] + ring, Gp.R[a] - 1);
+        const double e0 = Gp.lo[a] + (double)c0 * Gp.h[a] - Gp.eps, e1 = Gp.lo[a] + (double)(c1 + 1) * Gp.h[a] + Gp.eps;
+        const double d = fmax(fabs((double)q[a] - e0), fabs((double)q[a] - e1));
+        d2 += d * d;
+    }
+    return sqrt(d2) * 1.0001 + 1e-7;
+}
+
+// The 32*KP smallest of the n keys in buf, sorted ascending, back into
+// buf[0, 32*KP) (list order = the oracle's).  Instead of one bitonic sort of
+// all n keys rounded up to a power of two (112 register stages for
+// 64 < n <= 128), the first KP runs of 32 are sorted together and every later
+// run is folded in with the bitonic top-k merge: a run with no key below the
+// current (32*KP)-th smallest is skipped; otherwise it is sorted (15 stages),
+// reversed, min-combined with the top list's last 32 entries -- which leaves
+// the 32*KP smallest as a bitonic sequence -- and merged (5*KP + 1 stages).
+template <int KP>
+__device__ __forceinline__ void select_topk(uint64_t *buf, int n, unsigned lane) {
+    uint64_t top[KP];
+#pragma unroll
+    for (int sI = 0; sI < KP; ++sI) {
+        const int i = sI * 32 + (int)lane;
+        top[sI] = i < n ? buf[i] : ~0ull;
+    }
+    warp_sort_regs<KP>(top, lane);
+    for (int run = KP; run * 32 < n; ++run) {
+        const int i = run * 32 + (int)lane;
+        uint64_t x[1] = {i < n ? buf[i] : ~0ull};
+        const uint64_t kth = __shfl_sync(0xffffffffu, top[KP - 1], 31);
+        if (!__any_sync(0xffffffffu, x[0] < kth)) continue;
+        warp_sort_regs<1>(x, lane);
+        const uint64_t rev = __shfl_sync(0xffffffffu, x[0], 31 - (int)lane);
+        top[KP - 1] = rev < top[KP - 1] ? rev : top[KP - 1];
+        warp_bitonic_stage<KP>(top, lane, 0, 32 * KP, 16 * KP);
+    }
+    __syncwarp();  // every lane has read its keys before the list overwrites them
+#pragma unroll
+    for (int sI = 0; sI < KP; ++sI) buf[sI * 32 + (int)lane] = top[sI];
+    __syncwarp();
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnParams P) {
     __shared__ uint64_t s_keys[kSelWarps][kSelCap];
@@ -490,16 +554,19 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 const float d = q[a] < l ? l - q[a] : (q[a] > u ? q[a] - u : 0.0f);
                 return d * d;
             };
-            // 1. density probe (cell counts only)
+            // 1. density probe (cell counts only): cubes of half-size 0, 1, 2, 4, ...
+            // cells (geometric, so a query far from the photons -- an empty corner
+            // of a traced map -- costs O(ring^2) row reads, not O(ring^3)), rows
+            // clamped to the grid
             int ring = 0;
             uint32_t cube = 0;
-            for (;; ++ring) {
-                const int side = 2 * ring + 1;
+            for (;;) {
                 uint32_t c = 0;
                 const int x0 = max(qc[0] - ring, 0), x1 = min(qc[0] + ring, R[0] - 1);
-                for (int r = (int)lane; r < side * side; r += 32) {
-                    const int cz = qc[2] - ring + r / side, cy = qc[1] - ring + r % side;
-                    if (cz < 0 || cz >= R[2] || cy < 0 || cy >= R[1]) continue;
+                const int y0 = max(qc[1] - ring, 0), ny = min(qc[1] + ring, R[1] - 1) - y0 + 1;
+                const int z0 = max(qc[2] - ring, 0), nz = min(qc[2] + ring, R[2] - 1) - z0 + 1;
+                for (int r = (int)lane; r < ny * nz; r += 32) {
+                    const int cz = z0 + r / ny, cy = y0 + r % ny;
                     const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
                     c += __ldg(P.cell_start + row + x1 + 1) - __ldg(P.cell_start + row + x0);
                 }
@@ -507,6 +574,7 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
                 cube = c;
                 if (cube >= (uint32_t)K || ring >= rmax) break;
+                ring = min(ring == 0 ? 1 : 2 * ring, rmax);
             }
             double vol = 1.0;
 #pragma unroll
@@ -523,11 +591,21 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 all += d * d;
             }
             all = sqrt(all) * 1.001 + 1e-6;
+            // queries outside the phase's grid box (make_batch draws x ~ U^3 while a
+            // traced map fills only the medium): no photon is closer than dbox, and
+            // the probe measured the density at the box face nearest q
+            const double dbox = knn_box_dist(Gp, q);
+            // growth cap: the ball around the probe cube holds >= K photons
+            const double reach = cube >= (uint32_t)K ? fmin(knn_cube_reach(Gp, q, qc, ring), all) : all;
+            rho = fmin(rho + dbox, reach);
+            // bracket: a ball of radius lo_r held fewer than K photons, one of
+            // radius hi_r overflowed the buffer; proposals outside it bisect
+            double lo_r = dbox * (1.0 - 1e-6), hi_r = 3.0e38;
             // 2. collect every photon with d2 <= thr
             for (int attempt = 0;; ++attempt) {
                 const float rho2 = (float)fmin(rho * rho, 3.0e38);
                 const float thr = fminf(rho2, P.r2);
-                const int rc = (int)fmin(ceil(rho / (double)Gp.hmin) + 1.0, (double)rmax);
+                const int rc = (int)fmin(ceil(sqrt((double)thr) / (double)Gp.hmin) + 1.0, (double)rmax);
                 const int z0 = max(qc[2] - rc, 0), z1 = min(qc[2] + rc, R[2] - 1);
                 const int y0 = max(qc[1] - rc, 0), y1 = min(qc[1] + rc, R[1] - 1);
                 const int xl = max(qc[0] - rc, 0), xr = min(qc[0] + rc, R[0] - 1);
@@ -591,13 +669,19 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                     if (n > kSelCap) over = true;
                 }
                 const bool short_ = n < K && thr < P.r2 && rho < all;
-                // resize the ball from what this one held (density-corrected)
-                if (over && attempt < 10) {
-                    rho *= fmax(0.5, fmin(0.9, cbrt(1.3 * (double)K / (double)n)));
+                // resize the ball from what this one held (density-corrected), bisecting
+                // the bracket when the count is too steep in rho for the cube-root rule
+                if (over && attempt < kKnnAttempts) {
+                    hi_r = rho;
+                    const double nx = rho * fmax(0.5, fmin(0.9, cbrt(1.3 * (double)K / (double)n)));
+                    rho = nx > lo_r ? nx : 0.5 * (lo_r + hi_r);
                     continue;
                 }
-                if (short_ && attempt < 10) {
-                    rho = fmin(rho * fmin(3.0, fmax(1.25, cbrt(1.3 * (double)K / fmax((double)n, 1.0)))), all);
+                if (short_ && attempt < kKnnAttempts) {
+                    lo_r = rho;
+                    const double nx =
+                        fmin(rho * fmin(3.0, fmax(1.25, cbrt(1.3 * (double)K / fmax((double)n, 1.0)))), fmax(reach, rho));
+                    rho = nx < hi_r ? nx : 0.5 * (lo_r + hi_r);
                     continue;
                 }
                 fail = over || short_;
@@ -605,11 +689,8 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
             }
             __syncwarp();
             if (!fail) {
-                // 3. warp bitonic sort of the n keys in registers
-                if (n <= 32) sort_buf<1>(buf, n, lane);
-                else if (n <= 64) sort_buf<2>(buf, n, lane);
-                else if (n <= 128) sort_buf<4>(buf, n, lane);
-                else sort_buf<8>(buf, n, lane);
+                // 3. the K <= 32*KP smallest keys, sorted (bitonic top-k in registers)
+                select_topk<KP>(buf, n, lane);
                 count = min(n, K);
             }
         }
@@ -792,17 +873,17 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 return d * d;
             };
             // 1. density probe: smallest cube of cells around qc holding >= K photons
-            int ring = 0;
+            int ring = 0;  // half-sizes 0, 1, 2, 4, ... (as in k_knn_query_sel)
             unsigned long long cube = 0;
-            for (;; ++ring) {
+            for (;;) {
                 if (tid == 0) s_cube = 0ull;
                 __syncthreads();
-                const int side = 2 * ring + 1;
-                for (int r = tid; r < side * side; r += kCtaThreads) {
-                    const int cz = qc[2] - ring + r / side, cy = qc[1] - ring + r % side;
-                    if (cz < 0 || cz >= R[2] || cy < 0 || cy >= R[1]) continue;
+                const int x0 = max(qc[0] - ring, 0), x1 = min(qc[0] + ring, R[0] - 1);
+                const int y0 = max(qc[1] - ring, 0), ny = min(qc[1] + ring, R[1] - 1) - y0 + 1;
+                const int z0 = max(qc[2] - ring, 0), nz = min(qc[2] + ring, R[2] - 1) - z0 + 1;
+                for (int r = tid; r < ny * nz; r += kCtaThreads) {
+                    const int cz = z0 + r / ny, cy = y0 + r % ny;
                     const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
-                    const int x0 = max(qc[0] - ring, 0), x1 = min(qc[0] + ring, R[0] - 1);
                     atomicAdd(&s_cube, (unsigned long long)(__ldg(P.cell_start + row + x1 + 1) -
                                                            __ldg(P.cell_start + row + x0)));
                 }
@@ -810,6 +891,7 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 cube = s_cube;
                 __syncthreads();
                 if (cube >= (unsigned long long)K || ring >= rmax) break;
+                ring = min(ring == 0 ? 1 : 2 * ring, rmax);
             }
             // 2. radius whose ball should hold ~1.3 K photons (cube volume / count)
             double vol = 1.0;
@@ -828,11 +910,15 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 all += d * d;
             }
             all = sqrt(all) * 1.001 + 1e-6;
+            const double dbox = knn_box_dist(Gp, q);  // as in k_knn_query_sel
+            const double reach = cube >= (unsigned long long)K ? fmin(knn_cube_reach(Gp, q, qc, ring), all) : all;
+            rho = fmin(rho + dbox, reach);
+            double lo_r = dbox * (1.0 - 1e-6), hi_r = 3.0e38;
             for (int attempt = 0;; ++attempt) {
                 // 3. collect every photon with d2 <= thr
                 const float rho2 = (float)fmin(rho * rho, 3.0e38);
                 const float thr = fminf(rho2, P.r2);
-                const int rc = (int)fmin(ceil(rho / (double)Gp.hmin) + 1.0, (double)rmax);
+                const int rc = (int)fmin(ceil(sqrt((double)thr) / (double)Gp.hmin) + 1.0, (double)rmax);
                 if (tid == 0) {
                     s_n = 0;
                     s_over = 0;
@@ -872,12 +958,15 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 const bool over = s_over != 0;
                 const bool short_ = n < K && thr < P.r2 && rho < all;
                 __syncthreads();
-                if (over && attempt < 12) {
-                    rho *= 0.8;
+                if (over && attempt < kKnnAttempts) {
+                    hi_r = rho;
+                    rho = 0.8 * rho > lo_r ? 0.8 * rho : 0.5 * (lo_r + hi_r);
                     continue;
                 }
-                if (short_ && attempt < 12) {
-                    rho = fmin(rho * 1.5, all);
+                if (short_ && attempt < kKnnAttempts) {
+                    lo_r = rho;
+                    const double nx = fmin(rho * 1.5, fmax(reach, rho));
+                    rho = nx < hi_r ? nx : 0.5 * (lo_r + hi_r);
                     continue;
                 }
                 if (over || short_) {

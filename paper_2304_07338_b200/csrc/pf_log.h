@@ -108,7 +108,23 @@ PF_LOG_HD double pf_log_mul(double a, double b) {
 // log(y * 2^escale) for y a positive normal double and y * 2^escale normal: the same
 // operations as pf_log(y * 2^escale), with escale folded into the exponent k only, so
 // the result is bit-identical (z, r and the table index do not depend on escale).
-PF_LOG_HD double pf_log_scaled(double y, int escale) {
+#if defined(__CUDA_ARCH__)
+// Table entry i: from the read-only global table, or (SMEM) from a copy the
+// caller placed in shared memory at byte address tab (16-byte entries).
+template <bool SMEM>
+__device__ __forceinline__ double2 pf_log_tab_load(uint32_t i, uint32_t tab) {
+    if constexpr (SMEM) {
+        double2 v;
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(tab + 16u * i));
+        return v;
+    } else {
+        return __ldg(reinterpret_cast<const double2 *>(pf_log_tab_dev) + i);
+    }
+}
+#endif
+
+template <bool SMEM = false>
+PF_LOG_HD double pf_log_scaled(double y, int escale, uint32_t tab = 0u) {
     const uint64_t ix = pf_log_bits(y);
     const uint32_t hx = (uint32_t)(ix >> 32);
     const uint32_t tmp = hx - PF_LOG_OFF_HI;
@@ -118,13 +134,14 @@ PF_LOG_HD double pf_log_scaled(double y, int escale) {
 #if defined(__CUDA_ARCH__)
     pf_log_entry e;  // one 16-byte load
     {
-        const double2 v = __ldg(reinterpret_cast<const double2 *>(pf_log_tab_dev) + i);
+        const double2 v = pf_log_tab_load<SMEM>(i, tab);
         e.logc_hi = v.x;
         const unsigned long long u = (unsigned long long)__double_as_longlong(v.y);
         e.invc_hi = (uint32_t)u;
         e.logc_lo_hi = (uint32_t)(u >> 32);
     }
 #else
+    (void)tab;
     const pf_log_entry e = pf_log_tab_host[i];
 #endif
     const double z = pf_log_dbl(((uint64_t)(hx - ((uint32_t)kraw << 20)) << 32) | (ix & 0xffffffffull));
@@ -152,6 +169,6 @@ PF_LOG_HD double pf_log_scaled(double y, int escale) {
     return pf_log_add(hi, pf_log_add(lo, tail));
 }
 
-PF_LOG_HD double pf_log(double y) { return pf_log_scaled(y, 0); }
+PF_LOG_HD double pf_log(double y) { return pf_log_scaled<false>(y, 0); }
 
 }  // namespace pfk

@@ -44,7 +44,12 @@ __device__ __forceinline__ void par_flight(const DevScene &S, const double o[3],
 // -- bit-identical to pf_log(1.0 - pcg_double(r)), two binary64 ops cheaper.
 __device__ __forceinline__ double par_step(Pcg &r, double inv) {
     const uint64_t m = (1ull << 53) - (pcg_u64(r) >> 11);
-    return pf_log_scaled((double)m, -53) * inv;
+    return pf_log_scaled<false>((double)m, -53) * inv;
+}
+// the same with pf_log's table read from a shared-memory copy at byte address tab
+__device__ __forceinline__ double par_step_smem(Pcg &r, double inv, uint32_t tab) {
+    const uint64_t m = (1ull << 53) - (pcg_u64(r) >> 11);
+    return pf_log_scaled<true>((double)m, -53, tab) * inv;
 }
 
 // next_double() * sigma_max with one multiply: sm53 = sigma_max * 2^-53.

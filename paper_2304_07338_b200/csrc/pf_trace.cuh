@@ -122,6 +122,9 @@ __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3],
 #ifndef PF_PAR_CTAS
 #define PF_PAR_CTAS 7  // resident CTAs per SM (register budget 65536 / (128 x 7) = 73)
 #endif
+#ifndef PF_PAR_LOG_SMEM
+#define PF_PAR_LOG_SMEM 1  // 1: the step's log table from a per-CTA shared-memory copy (LDS) instead of LDG
+#endif
 __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
     k_render_trace_parity(const DevScene S, const TraceParams P) {
     double *slots = reinterpret_cast<double *>(P.slots);
@@ -147,6 +150,13 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
     __shared__ float2 s_qb[PF_TRACE_THREADS];
     const ParFlightSmem Fm{s_qa, s_qb};
     const int tx = threadIdx.x;
+#if PF_PAR_LOG_SMEM
+    __shared__ double2 s_logtab[1 << PF_LOG_BITS];
+    for (int i = tx; i < (1 << PF_LOG_BITS); i += PF_TRACE_THREADS)
+        s_logtab[i] = reinterpret_cast<const double2 *>(pf_log_tab_dev)[i];
+    __syncthreads();
+    const uint32_t logtab = (uint32_t)__cvta_generic_to_shared(s_logtab);
+#endif
 
     // step-loop state: registers
     // 0 waiting for a sample, 1 primary flight, 2 shadow flight, 3 queue drained;
@@ -320,7 +330,11 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
             int ev = 0;  // 0 none, 1 left the segment, 2 parked at a voxel fetch
 #pragma unroll 1
             for (int k = 0; k < PF_PAR_BURST; ++k) {
+#if PF_PAR_LOG_SMEM
+                t -= par_step_smem(rng, inv_sm, logtab);
+#else
                 t -= par_step(rng, inv_sm);
+#endif
                 ++nstep;
                 if (t > t1) {
                     ev = 1;

@@ -126,3 +126,29 @@ def test_large_k_select_kernel_exact(ctx, oracle):
         for K, rad in [(1024, float("inf")), (257, float("inf")), (1024, 0.05), (100, 0.3)]:
             g = r.integers(0, 3, len(q)).astype(np.uint8)
             _check_against_brute(ctx, oracle, ph, q, g, K, rad)
+
+
+def _ball_map(n, seed):
+    """Traced-map stand-in: photons only inside a ball (r = 0.3, denser at the
+    centre) while make_batch queries fill the unit cube, so many queries sit in
+    empty corners or outside the phase's grid box (the bracketed radius search)."""
+    r = np.random.default_rng(seed)
+    d = r.standard_normal((n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    pos = 0.5 + d * (0.3 * r.random((n, 1)) ** 0.6)
+    dirs = r.standard_normal((n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    return make_photons(pos.astype(np.float32), dirs.astype(np.float32), r.random((n, 3)).astype(np.float32),
+                        r.integers(0, 3, n))
+
+
+@pytest.mark.parametrize("K,r", [(64, float("inf")), (64, 0.05), (32, 0.25), (1024, float("inf")), (100, 0.25)])
+def test_knn_ball_map_unit_cube_queries(ctx, oracle, K, r):
+    """Exact ids / d2 / counts on a clustered ball map with queries over the
+    whole unit cube (corners: nearest photons 0.3-0.6 away) and beyond it."""
+    ph = _ball_map(30000, 21)
+    ctx.knn_build(ph, PHASES)
+    rq = np.random.default_rng(22)
+    q = np.concatenate([rq.random((300, 3)), [[0.0, 0.0, 0.0], [1.0, 1.0, 1.0], [1.5, -0.5, 0.5]]]).astype(np.float32)
+    g = rq.integers(0, 3, len(q)).astype(np.uint8)
+    _check_against_brute(ctx, oracle, ph, q, g, K, r)
