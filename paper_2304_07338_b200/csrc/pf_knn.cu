@@ -554,10 +554,10 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 const float d = q[a] < l ? l - q[a] : (q[a] > u ? q[a] - u : 0.0f);
                 return d * d;
             };
-            // 1. density probe (cell counts only): cubes of half-size 0, 1, 2, 4, ...
-            // cells (geometric, so a query far from the photons -- an empty corner
-            // of a traced map -- costs O(ring^2) row reads, not O(ring^3)), rows
-            // clamped to the grid
+            // 1. density probe (cell counts only): cubes of half-size 0, 1, .., 4, 8,
+            // 16, ... cells (tight density estimate near the photons; geometric
+            // beyond, so a query far from them -- an empty corner of a traced map --
+            // costs O(ring^2) row reads, not O(ring^3)), rows clamped to the grid
             int ring = 0;
             uint32_t cube = 0;
             for (;;) {
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
                 cube = c;
                 if (cube >= (uint32_t)K || ring >= rmax) break;
-                ring = min(ring == 0 ? 1 : 2 * ring, rmax);
+                ring = min(ring < 4 ? ring + 1 : 2 * ring, rmax);
             }
             double vol = 1.0;
 #pragma unroll
@@ -597,10 +597,13 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
             const double dbox = knn_box_dist(Gp, q);
             // growth cap: the ball around the probe cube holds >= K photons
             const double reach = cube >= (uint32_t)K ? fmin(knn_cube_reach(Gp, q, qc, ring), all) : all;
-            rho = fmin(rho + dbox, reach);
-            // bracket: a ball of radius lo_r held fewer than K photons, one of
-            // radius hi_r overflowed the buffer; proposals outside it bisect
-            double lo_r = dbox * (1.0 - 1e-6), hi_r = 3.0e38;
+            // bracket: a ball of radius lo_r holds fewer than K photons -- beyond the
+            // box distance, the ball inside the previous (< K) probe cube when q is
+            // in the grid -- one of radius hi_r overflowed; proposals outside bisect
+            double lo_r = dbox > 0.0 ? dbox * (1.0 - 1e-6) : (double)(ring <= 4 ? max(ring - 1, 0) : ring >> 1) * (double)Gp.hmin * (1.0 - 1e-6);
+            double hi_r = 3.0e38;
+            rho = fmin(fmax(rho + dbox, lo_r), reach);
+            const float ihx = (float)Gp.inv_h[0];
             // 2. collect every photon with d2 <= thr
             for (int attempt = 0;; ++attempt) {
                 const float rho2 = (float)fmin(rho * rho, 3.0e38);
@@ -618,16 +621,21 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 // scan concatenates the row segments and all 32 lanes stream the
                 // concatenated candidates (independent, coalesced loads)
                 const int ny = y1 - y0 + 1, nrows = (z1 - z0 + 1) * ny;
+                // lane's row cursor (row r0 + lane), advanced 32 rows per chunk
+                int cz = z0 + (int)lane / ny, cy = y0 + (int)lane % ny;
+                const int dz32 = 32 / ny, dy32 = 32 % ny;
                 for (int r0 = 0; r0 < nrows && !over; r0 += 32) {
                     const int r = r0 + (int)lane;
                     uint32_t b = 0, len = 0;
                     if (r < nrows) {
-                        const int cz = z0 + r / ny, cy = y0 + r % ny;
                         const float gyz = gap(2, cz, cz) + gap(1, cy, cy);
                         if ((gyz + gx) * (1.0f - 1e-5f) <= thr) {
-                            const double dxm = sqrt((double)fmaxf(thr - gyz * (1.0f - 1e-5f), 0.0f)) * 1.00001 + 1e-7;
-                            const int xa = max(xl, cell_axis((double)q[0] - dxm, Gp.lo[0], Gp.inv_h[0], R[0]));
-                            const int xb = min(xr, cell_axis((double)q[0] + dxm, Gp.lo[0], Gp.inv_h[0], R[0]));
+                            // x-cells the ball reaches in this row: binary32 estimate of the
+                            // binning function floor((x - lo) / h) with a 1e-3-cell margin
+                            // (its rounding error is ~1e-4 cells), so the range is a superset
+                            const float dxm = sqrtf(fmaxf(thr - gyz * (1.0f - 1e-5f), 0.0f)) * 1.0001f + 1e-6f;
+                            const int xa = max(xl, (int)floorf((q[0] - dxm - lo[0]) * ihx - 1e-3f));
+                            const int xb = min(xr, (int)floorf((q[0] + dxm - lo[0]) * ihx + 1e-3f));
                             if (xa <= xb) {
                                 const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
                                 b = __ldg(P.cell_start + row + xa);
@@ -667,6 +675,12 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                         n += __popc(m);
                     }
                     if (n > kSelCap) over = true;
+                    cy += dy32;
+                    cz += dz32;
+                    if (cy > y1) {
+                        cy -= ny;
+                        ++cz;
+                    }
                 }
                 const bool short_ = n < K && thr < P.r2 && rho < all;
                 // resize the ball from what this one held (density-corrected), bisecting
@@ -873,7 +887,7 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 return d * d;
             };
             // 1. density probe: smallest cube of cells around qc holding >= K photons
-            int ring = 0;  // half-sizes 0, 1, 2, 4, ... (as in k_knn_query_sel)
+            int ring = 0;  // half-sizes 0..4, 8, 16, ... (as in k_knn_query_sel)
             unsigned long long cube = 0;
             for (;;) {
                 if (tid == 0) s_cube = 0ull;
@@ -891,7 +905,7 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 cube = s_cube;
                 __syncthreads();
                 if (cube >= (unsigned long long)K || ring >= rmax) break;
-                ring = min(ring == 0 ? 1 : 2 * ring, rmax);
+                ring = min(ring < 4 ? ring + 1 : 2 * ring, rmax);
             }
             // 2. radius whose ball should hold ~1.3 K photons (cube volume / count)
             double vol = 1.0;
@@ -912,8 +926,9 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
             all = sqrt(all) * 1.001 + 1e-6;
             const double dbox = knn_box_dist(Gp, q);  // as in k_knn_query_sel
             const double reach = cube >= (unsigned long long)K ? fmin(knn_cube_reach(Gp, q, qc, ring), all) : all;
-            rho = fmin(rho + dbox, reach);
-            double lo_r = dbox * (1.0 - 1e-6), hi_r = 3.0e38;
+            double lo_r = dbox > 0.0 ? dbox * (1.0 - 1e-6) : (double)(ring <= 4 ? max(ring - 1, 0) : ring >> 1) * (double)Gp.hmin * (1.0 - 1e-6);
+            double hi_r = 3.0e38;
+            rho = fmin(fmax(rho + dbox, lo_r), reach);
             for (int attempt = 0;; ++attempt) {
                 // 3. collect every photon with d2 <= thr
                 const float rho2 = (float)fmin(rho * rho, 3.0e38);

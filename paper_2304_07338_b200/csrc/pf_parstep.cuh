@@ -74,14 +74,20 @@ __device__ __forceinline__ ParFlight par_load(const ParFlightSmem &m, int tx) {
     return f;
 }
 
+// High word of the majorant bound of the cell holding x(t) (one TEX).
+__device__ __forceinline__ unsigned par_bound(const DevScene &S, const ParFlight &f, double t, double tb) {
+    const float s = (float)(t - tb);
+    return tex3D<unsigned>(S.maj_tex, fmaf(f.qd[0], s, f.qo[0]), fmaf(f.qd[1], s, f.qo[1]),
+                           fmaf(f.qd[2], s, f.qo[2]));
+}
+// u2sm >= 0: u2sm >= as_double(b, 0)  <=>  hi32(u2sm) >= b
+__device__ __forceinline__ bool par_null_given(double u2sm, unsigned b) {
+    return (uint32_t)((unsigned long long)__double_as_longlong(u2sm) >> 32) >= b;
+}
 // true => the reference certainly rejects this tentative collision.
 __device__ __forceinline__ bool par_certain_null(const DevScene &S, const ParFlight &f, double t, double tb,
                                                  double u2sm) {
-    const float s = (float)(t - tb);
-    const unsigned b = tex3D<unsigned>(S.maj_tex, fmaf(f.qd[0], s, f.qo[0]), fmaf(f.qd[1], s, f.qo[1]),
-                                       fmaf(f.qd[2], s, f.qo[2]));
-    // u2sm >= 0: u2sm >= as_double(b, 0)  <=>  hi32(u2sm) >= b
-    return (uint32_t)((unsigned long long)__double_as_longlong(u2sm) >> 32) >= b;
+    return par_null_given(u2sm, par_bound(S, f, t, tb));
 }
 
 }  // namespace pfk

@@ -114,13 +114,16 @@ __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3],
 #define PF_PAR_REFILL 4  // waiting lanes that trigger a refill from the warp queue
 #endif
 #ifndef PF_PAR_FETCH
-#define PF_PAR_FETCH 4  // lanes parked at a voxel fetch that trigger a fetch round
+#define PF_PAR_FETCH 2  // lanes parked at a voxel fetch that trigger a fetch round
 #endif
 #ifndef PF_PAR_BURST
 #define PF_PAR_BURST 16  // tentative collisions per lane between warp-level checks
 #endif
 #ifndef PF_PAR_CTAS
-#define PF_PAR_CTAS 7  // resident CTAs per SM (register budget 65536 / (128 x 7) = 73)
+#define PF_PAR_CTAS 5  // resident CTAs per SM (register budget 65536 / (128 x 5) = 102 for the pipelined burst)
+#endif
+#ifndef PF_PAR_PIPE
+#define PF_PAR_PIPE 1  // 1: software-pipelined burst (next step's log overlaps this step's TEX)
 #endif
 #ifndef PF_PAR_LOG_SMEM
 #define PF_PAR_LOG_SMEM 1  // 1: the step's log table from a per-CTA shared-memory copy (LDS) instead of LDG
@@ -156,6 +159,9 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
         s_logtab[i] = reinterpret_cast<const double2 *>(pf_log_tab_dev)[i];
     __syncthreads();
     const uint32_t logtab = (uint32_t)__cvta_generic_to_shared(s_logtab);
+#define PAR_STEP(r) par_step_smem(r, inv_sm, logtab)
+#else
+#define PAR_STEP(r) par_step(r, inv_sm)
 #endif
 
     // step-loop state: registers
@@ -328,13 +334,47 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
             const ParFlight F = par_load(Fm, tx);
             const double tb = s_tb[tx];
             int ev = 0;  // 0 none, 1 left the segment, 2 parked at a voxel fetch
+#if PF_PAR_PIPE
+            // Software-pipelined: step k+1's u1 draw and binary64 log are computed
+            // while step k's majorant TEX is in flight (they do not depend on it);
+            // if step k parks (or the burst ends) the speculative u1 draw is undone
+            // by restoring the stream state, so the RNG sequence and every
+            // decision are exactly the unpipelined ones.
+            t -= PAR_STEP(rng);
+            ++nstep;
+            if (t > t1) {
+                ev = 1;
+            } else {
+                double u2sm = par_u2sm(rng, sm53);
+                unsigned bnd = par_bound(S, F, t, tb);
+#pragma unroll 1
+                for (int k = 1;; ++k) {
+                    const unsigned long long saved = rng.state;
+                    const double tn = t - PAR_STEP(rng);  // speculative step k+1
+                    if (!par_null_given(u2sm, bnd)) {
+                        rng.state = saved;
+                        s_u2[tx] = u2sm;  // park until the warp's next fetch round
+                        ev = 2;
+                        break;
+                    }
+                    if (k == PF_PAR_BURST) {
+                        rng.state = saved;
+                        break;
+                    }
+                    t = tn;
+                    ++nstep;
+                    if (t > t1) {
+                        ev = 1;
+                        break;
+                    }
+                    u2sm = par_u2sm(rng, sm53);
+                    bnd = par_bound(S, F, t, tb);
+                }
+            }
+#else
 #pragma unroll 1
             for (int k = 0; k < PF_PAR_BURST; ++k) {
-#if PF_PAR_LOG_SMEM
-                t -= par_step_smem(rng, inv_sm, logtab);
-#else
-                t -= par_step(rng, inv_sm);
-#endif
+                t -= PAR_STEP(rng);
                 ++nstep;
                 if (t > t1) {
                     ev = 1;
@@ -349,6 +389,7 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
                     break;
                 }
             }
+#endif
             if (ev == 0) continue;
             if (ev == 2) {
                 phase |= 4;
