@@ -486,6 +486,26 @@ __device__ __forceinline__ double knn_cube_reach(const KnnGrid &Gp, const float 
     return sqrt(d2) * 1.0001 + 1e-7;
 }
 
+// binary32 versions for the warp kernel, whose per-query radius bookkeeping
+// otherwise costs ~8% of its instructions in binary64: lo/h/eps are the
+// kernel's float copies of the grid, and every bound carries a relative margin
+// in the safe direction (the bounds only steer the search; the collection test
+// itself is exact).  ring < 0: the whole grid box; inner: distance to the box
+// instead of to its farthest corner.
+__device__ __forceinline__ float knn_extent_f(const float lo[3], const float h[3], const int R[3], float eps,
+                                              const float q[3], const int qc[3], int ring, bool inner) {
+    float d2 = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int c0 = ring < 0 ? 0 : max(qc[a] - ring, 0), c1 = ring < 0 ? R[a] - 1 : min(qc[a] + ring, R[a] - 1);
+        const float e0 = fmaf((float)c0, h[a], lo[a]) - eps, e1 = fmaf((float)(c1 + 1), h[a], lo[a]) + eps;
+        const float d = inner ? (q[a] < e0 ? e0 - q[a] : (q[a] > e1 ? q[a] - e1 : 0.0f))
+                              : fmaxf(fabsf(q[a] - e0), fabsf(q[a] - e1));
+        d2 = fmaf(d, d, d2);
+    }
+    return sqrtf(d2);
+}
+
 // The 32*KP smallest of the n keys in buf, sorted ascending, back into
 // buf[0, 32*KP) (list order = the oracle's).  Instead of one bitonic sort of
 // all n keys rounded up to a power of two (112 register stages for
@@ -546,6 +566,7 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 qc[a] = cell_axis((double)q[a], Gp.lo[a], Gp.inv_h[a], R[a]);
             }
             const float eps = (float)Gp.eps + 1e-6f;
+            const float hminf = (float)Gp.hmin;
             const uint32_t cbase = Gp.cell_base;
             const int rmax = max(R[0], max(R[1], R[2]));
             auto gap = [&](int a, int c0, int c1) -> float {
@@ -576,39 +597,33 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 if (cube >= (uint32_t)K || ring >= rmax) break;
                 ring = min(ring < 4 ? ring + 1 : 2 * ring, rmax);
             }
-            double vol = 1.0;
+            float vol = 1.0f;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int c0 = max(qc[a] - ring, 0), c1 = min(qc[a] + ring, R[a] - 1);
-                vol *= (double)(c1 - c0 + 1) * (double)h[a];
+                vol *= (float)(c1 - c0 + 1) * h[a];
             }
-            double rho = cbrt(1.3 * (double)K * vol / (fmax((double)cube, 1.0) * 4.18879020478639098));
-            double all = 0.0;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const double b0 = Gp.lo[a] - Gp.eps, b1 = Gp.lo[a] + (double)R[a] * Gp.h[a] + Gp.eps;
-                const double d = fmax(fabs((double)q[a] - b0), fabs((double)q[a] - b1));
-                all += d * d;
-            }
-            all = sqrt(all) * 1.001 + 1e-6;
+            float rho = cbrtf(1.3f * (float)K * vol / (fmaxf((float)cube, 1.0f) * 4.18879020f));
+            // a radius whose ball holds every photon of the phase (grid box + slack)
+            const float all = knn_extent_f(lo, h, R, eps, q, qc, -1, false) * 1.001f + 1e-6f;
             // queries outside the phase's grid box (make_batch draws x ~ U^3 while a
             // traced map fills only the medium): no photon is closer than dbox, and
             // the probe measured the density at the box face nearest q
-            const double dbox = knn_box_dist(Gp, q);
+            const float dbox = knn_extent_f(lo, h, R, eps, q, qc, -1, true) * (1.0f - 1e-5f);
             // growth cap: the ball around the probe cube holds >= K photons
-            const double reach = cube >= (uint32_t)K ? fmin(knn_cube_reach(Gp, q, qc, ring), all) : all;
+            const float reach =
+                cube >= (uint32_t)K ? fminf(knn_extent_f(lo, h, R, eps, q, qc, ring, false) * 1.0001f + 1e-6f, all) : all;
             // bracket: a ball of radius lo_r holds fewer than K photons -- beyond the
             // box distance, the ball inside the previous (< K) probe cube when q is
             // in the grid -- one of radius hi_r overflowed; proposals outside bisect
-            double lo_r = dbox > 0.0 ? dbox * (1.0 - 1e-6) : (double)(ring <= 4 ? max(ring - 1, 0) : ring >> 1) * (double)Gp.hmin * (1.0 - 1e-6);
-            double hi_r = 3.0e38;
-            rho = fmin(fmax(rho + dbox, lo_r), reach);
+            float lo_r = dbox > 0.0f ? dbox : (float)(ring <= 4 ? max(ring - 1, 0) : ring >> 1) * hminf * (1.0f - 1e-5f);
+            float hi_r = 3.0e38f;
+            rho = fminf(fmaxf(rho + dbox, lo_r), reach);
             const float ihx = (float)Gp.inv_h[0];
             // 2. collect every photon with d2 <= thr
             for (int attempt = 0;; ++attempt) {
-                const float rho2 = (float)fmin(rho * rho, 3.0e38);
-                const float thr = fminf(rho2, P.r2);
-                const int rc = (int)fmin(ceil(sqrt((double)thr) / (double)Gp.hmin) + 1.0, (double)rmax);
+                const float thr = fminf(fminf(rho * rho, 3.0e38f), P.r2);
+                const int rc = (int)fminf(ceilf(sqrtf(thr) * 1.00001f / hminf) + 1.0f, (float)rmax);
                 const int z0 = max(qc[2] - rc, 0), z1 = min(qc[2] + rc, R[2] - 1);
                 const int y0 = max(qc[1] - rc, 0), y1 = min(qc[1] + rc, R[1] - 1);
                 const int xl = max(qc[0] - rc, 0), xr = min(qc[0] + rc, R[0] - 1);
@@ -687,15 +702,15 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                 // the bracket when the count is too steep in rho for the cube-root rule
                 if (over && attempt < kKnnAttempts) {
                     hi_r = rho;
-                    const double nx = rho * fmax(0.5, fmin(0.9, cbrt(1.3 * (double)K / (double)n)));
-                    rho = nx > lo_r ? nx : 0.5 * (lo_r + hi_r);
+                    const float nx = rho * fmaxf(0.5f, fminf(0.9f, cbrtf(1.3f * (float)K / (float)n)));
+                    rho = nx > lo_r ? nx : 0.5f * (lo_r + hi_r);
                     continue;
                 }
                 if (short_ && attempt < kKnnAttempts) {
                     lo_r = rho;
-                    const double nx =
-                        fmin(rho * fmin(3.0, fmax(1.25, cbrt(1.3 * (double)K / fmax((double)n, 1.0)))), fmax(reach, rho));
-                    rho = nx < hi_r ? nx : 0.5 * (lo_r + hi_r);
+                    const float nx =
+                        fminf(rho * fminf(3.0f, fmaxf(1.25f, cbrtf(1.3f * (float)K / fmaxf((float)n, 1.0f)))), fmaxf(reach, rho));
+                    rho = nx < hi_r ? nx : 0.5f * (lo_r + hi_r);
                     continue;
                 }
                 fail = over || short_;

@@ -52,18 +52,33 @@ __device__ __forceinline__ bool track(const DevScene &S, const double o[3], cons
     const double inv = S.inv_sigma_max, sm53 = S.sm53;
     ParFlight F;
     par_flight(S, o, d, t0, F);
-    double t = t0;
+    // software-pipelined like the render tracer: the next step's u1 draw and
+    // log run while this step's majorant TEX is in flight; a real collision
+    // undoes the speculative draw, a rejected fetch keeps it (it is exactly
+    // the reference's next draw)
+    double t = t0 - par_step(rng, inv);
+    if (t > t1) return false;
+    ++steps;
+    double u2sm = par_u2sm(rng, sm53);
+    unsigned bnd = par_bound(S, F, t, t0);
     for (;;) {
-        t -= par_step(rng, inv);
+        const unsigned long long saved = rng.state;
+        const double tn = t - par_step(rng, inv);
+        if (!par_null_given(u2sm, bnd)) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) x[a] = o[a] + d[a] * t;
+            const double s = sample_d(S, x);
+            tf_rgba_d(S, s, c);
+            if (u2sm < S.density_scale * c[3]) {
+                rng.state = saved;
+                return true;
+            }
+        }
+        t = tn;
         if (t > t1) return false;
         ++steps;
-        const double u2sm = par_u2sm(rng, sm53);
-        if (par_certain_null(S, F, t, t0, u2sm)) continue;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) x[a] = o[a] + d[a] * t;
-        const double s = sample_d(S, x);
-        tf_rgba_d(S, s, c);
-        if (u2sm < S.density_scale * c[3]) return true;
+        u2sm = par_u2sm(rng, sm53);
+        bnd = par_bound(S, F, t, t0);
     }
 }
 
