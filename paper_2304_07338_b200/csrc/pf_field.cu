@@ -67,19 +67,31 @@ __device__ __forceinline__ void st_feats_global(uint8_t *p, const float *acc) {
     else __stcs(reinterpret_cast<unsigned int *>(p), h[0]);
 }
 
-// K3: hash-grid encoding, one thread per (query, unit); a warp covers 8
-// queries x 4 units so each level's 8 rows land as one contiguous 128-byte
-// store.  Units: pos levels, dir levels, then one "g + zero padding" unit.
+#ifndef PF_ENC_G
+#define PF_ENC_G 2
+#endif
+static_assert(PF_ENC_G == 2 || PF_ENC_G == 4 || PF_ENC_G == 8, "levels per encoder sweep: 2, 4 or 8");
+
+// K3: hash-grid encoding, one thread per (query, unit); a warp covers 16
+// queries x 2 units (PF_ENC_G units per level-major sweep: A/B 2 < 4 < 8 by
+// 3% / 9%, the hash tables in use stay L2-resident) so each level's rows land
+// as contiguous 128-byte stores.  Units: pos levels, dir levels, then one
+// "g + zero padding" unit.  6 CTAs of 256 per SM (42 registers).
+#ifndef PF_ENC_MINB
+#define PF_ENC_MINB 6
+#endif
 template <int FP, int FD>
-__global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
+__global__ void __launch_bounds__(256, PF_ENC_MINB) k_field_encode(const FieldParams P) {
     const size_t n_all = P.mode == 0 ? (size_t)(*P.n_hits) : P.n_query;
     const size_t n = n_all > P.row0 ? min(n_all - P.row0, P.row_cap) : 0;  // rows of this launch
     const size_t n_rows = (n + 127) & ~(size_t)127;  // whole tiles (pad rows encode zeros)
-    const int U = P.n_pos_levels + P.n_dir_levels + 1, U4 = (U + 3) >> 2;
+    // PF_ENC_G levels per sweep (a warp covers 32 / G rows x G levels)
+    constexpr int G = PF_ENC_G, RW = 32 / G;
+    const int U = P.n_pos_levels + P.n_dir_levels + 1, UG = (U + G - 1) / G;
     const int lane = threadIdx.x & 31;
     const uint32_t warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t n_rg = (uint32_t)(n_rows >> 3);  // 8-row groups (< 2^29: render rows < 2^32)
+    const uint32_t n_rg = (uint32_t)(n_rows / RW);  // RW-row groups (render rows < 2^32)
     // per-level addressing in shared memory: each warp reads 4 different
     // levels, which a dynamically indexed kernel-parameter load serialises
     __shared__ FieldLevel s_lv[PF_FIELD_MAX_LEVELS];
@@ -88,10 +100,10 @@ __global__ void __launch_bounds__(256) k_field_encode(const FieldParams P) {
     // level-major: the whole grid sweeps all rows for one group of 4 levels
     // before the next, so the tables in use (4 x <= 8 MB at the paper config)
     // stay L2-resident instead of being gathered from DRAM
-    for (int ug = 0; ug < U4; ++ug)
+    for (int ug = 0; ug < UG; ++ug)
     for (uint32_t rg = warp0; rg < n_rg; rg += n_warps) {
-        const size_t row = (size_t)rg * 8 + (lane & 7);
-        const int u = ug * 4 + (lane >> 3);
+        const size_t row = (size_t)rg * RW + (lane % RW);
+        const int u = ug * G + lane / RW;
         if (u >= U) continue;
         const bool valid = row < n;
         const size_t gr = P.row0 + row;  // global item index

@@ -870,7 +870,7 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
     double *terms = reinterpret_cast<double *>(keys);  // 3 x 1024, keys are dead once `sel` is sorted
     __shared__ int s_n, s_over, s_cnt;
     __shared__ uint64_t s_prefix;
-    __shared__ int s_need;
+    __shared__ int s_need, s_unique;
     __shared__ unsigned long long s_cube;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int K = P.K;
@@ -1003,12 +1003,17 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                     count = -1;  // give up (never observed): the warp kernel redoes this query
                     break;
                 }
-                // 4. K-th smallest key (radix select, MSD 8 bits at a time)
+                // 4. K-th smallest key (radix select, MSD 8 bits at a time); stops
+                // as soon as the K-th key's bin holds it alone: the selection is then
+                // "prefix <= the K-th key's prefix" (the first 2-3 passes for
+                // distinct distances instead of all 8)
                 count = min(n, K);
+                uint64_t kmask = ~0ull;
                 if (n > K) {
                     if (tid == 0) {
                         s_prefix = 0ull;
                         s_need = K;
+                        s_unique = 0;
                     }
                     for (int pass = 0; pass < 8; ++pass) {
                         const int shift = 56 - 8 * pass;
@@ -1049,11 +1054,16 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                                 }
                                 s_need = left;
                                 s_prefix = pre | ((uint64_t)bsel << shift);
+                                s_unique = hist[bsel] == 1u ? 1 : 0;
                             }
                         }
                         __syncthreads();
+                        if (s_unique) {
+                            kmask = ~0ull << shift;
+                            break;
+                        }
                     }
-                    kth = s_prefix;  // keys are distinct: the K-th key itself
+                    kth = s_prefix;  // with kmask: the K-th key's prefix (keys are distinct)
                 } else {
                     kth = ~0ull;
                 }
@@ -1061,7 +1071,7 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 if (tid == 0) s_cnt = 0;
                 __syncthreads();
                 for (int i = tid; i < n; i += kCtaThreads)
-                    if (keys[i] <= kth) sel[atomicAdd(&s_cnt, 1)] = keys[i];
+                    if ((keys[i] & kmask) <= kth) sel[atomicAdd(&s_cnt, 1)] = keys[i];
                 __syncthreads();
                 int P2 = 32;
                 while (P2 < count) P2 <<= 1;

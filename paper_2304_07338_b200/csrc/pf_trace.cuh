@@ -111,7 +111,7 @@ __device__ __forceinline__ void nee_term(const DevScene &S, int l, const R x[3],
 // keeps the step loop spill-free and short (~100 instructions vs ~280).
 // ---------------------------------------------------------------------------
 #ifndef PF_PAR_REFILL
-#define PF_PAR_REFILL 4  // waiting lanes that trigger a refill from the warp queue
+#define PF_PAR_REFILL 2  // waiting lanes that trigger a refill from the warp queue
 #endif
 #ifndef PF_PAR_FETCH
 #define PF_PAR_FETCH 2  // lanes parked at a voxel fetch that trigger a fetch round
