@@ -76,7 +76,7 @@ static_assert(PF_ENC_G == 2 || PF_ENC_G == 4 || PF_ENC_G == 8, "levels per encod
 // queries x 2 units (PF_ENC_G units per level-major sweep: A/B 2 < 4 < 8 by
 // 3% / 9%, the hash tables in use stay L2-resident) so each level's rows land
 // as contiguous 128-byte stores.  Units: pos levels, dir levels, then one
-// "g + zero padding" unit.  6 CTAs of 256 per SM (42 registers).
+// "g + zero padding" unit.  6 CTAs of 256 per SM (40 registers).
 #ifndef PF_ENC_MINB
 #define PF_ENC_MINB 6
 #endif
