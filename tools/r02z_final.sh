@@ -33,5 +33,6 @@ ncu -i $O/knn_sel.ncu-rep --page source --csv --print-source cuda,sass -k regex:
 python tools/ncu_lines.py $O/knn_src.csv 1048576 40 > $O/prof/lines_knn_sel.txt 2>&1
 python tools/ncu_hotspots.py $O/frame_par.ncu-rep k_field_mlp > $O/prof/hot_field_mlp.md 2>&1
 python tools/ncu_hotspots.py $O/trace_fast.ncu-rep k_render_trace_fast > $O/prof/hot_trace_fast.md 2>&1
-cp $O/frame_par.ncu-rep $O/prof/ 2>/dev/null
+# only the summaries travel back (gpurun_out is capped at 64 MiB)
+rm -f $O/*.ncu-rep $O/par_src.csv $O/knn_src.csv
 ls -la $O/prof
