@@ -24,6 +24,10 @@
 
 #include "pf_log_table.h"
 
+#ifndef PF_LOG_I2F
+#define PF_LOG_I2F 1  // 0: round-1 instruction choices (A/B)
+#endif
+
 #if defined(__CUDACC__)
 #define PF_LOG_HD __host__ __device__ __forceinline__
 #else
@@ -147,8 +151,12 @@ PF_LOG_HD double pf_log_scaled(double y, int escale, uint32_t tab = 0u) {
     const double z = pf_log_dbl(((uint64_t)(hx - ((uint32_t)kraw << 20)) << 32) | (ix & 0xffffffffull));
     const double invc = pf_log_dbl((uint64_t)e.invc_hi << 32);
     const double logc_lo = pf_log_dbl((uint64_t)e.logc_lo_hi << 32);
+#if defined(__CUDA_ARCH__) && PF_LOG_I2F
+    const double kd = __int2double_rn(k);  // exact; one I2F on the XU pipe (~20% busy) beats 3 ALU/DP ops
+#else
     // kd = (double)k without a conversion instruction: 2^52 + (k + 1024) - (2^52 + 1024)
     const double kd = pf_log_sub(pf_log_dbl(0x4330000000000000ull | (uint32_t)(k + 1024)), 0x1.0000000000400p52);
+#endif
     const double r = pf_log_fma(z, invc, -1.0);                    // exact
     const double w = pf_log_fma(kd, PF_LOG_C(7), e.logc_hi);       // exact
     // TwoSum(w, r)
@@ -157,8 +165,14 @@ PF_LOG_HD double pf_log_scaled(double y, int escale, uint32_t tab = 0u) {
     const double lo = pf_log_add(pf_log_sub(w, pf_log_sub(hi, bb)), pf_log_sub(r, bb));
     // log1p(r) - r = r^2 (c2 + c3 r + ... + c8 r^6)
     const double r2 = pf_log_mul(r, r);
+    // -1/8 as a literal: an exact short DFMA immediate, so the first step needs
+    // no register copy of a constant-bank operand
+#if PF_LOG_I2F
+    double p = pf_log_fma(r, -0.125, PF_LOG_C(1));  // -1/8 r + 1/7
+#else
     double p = PF_LOG_C(0);                 // -1/8
     p = pf_log_fma(p, r, PF_LOG_C(1));      // 1/7
+#endif
     p = pf_log_fma(p, r, PF_LOG_C(2));      // -1/6
     p = pf_log_fma(p, r, PF_LOG_C(3));      // 1/5
     p = pf_log_fma(p, r, PF_LOG_C(4));      // -1/4
