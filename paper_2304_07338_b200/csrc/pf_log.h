@@ -112,17 +112,16 @@ PF_LOG_HD double pf_log_mul(double a, double b) {
 // log(y * 2^escale) for y a positive normal double and y * 2^escale normal: the same
 // operations as pf_log(y * 2^escale), with escale folded into the exponent k only, so
 // the result is bit-identical (z, r and the table index do not depend on escale).
-#if defined(__CUDA_ARCH__)
-// Table entry i: from the read-only global table, or (SMEM) from a copy the
-// caller placed in shared memory at byte address tab (16-byte entries).
-template <bool SMEM>
-__device__ __forceinline__ double2 pf_log_tab_load(uint32_t i, uint32_t tab) {
-    if constexpr (SMEM) {
-        double2 v;
-        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(tab + 16u * i));
-        return v;
-    } else {
-        return __ldg(reinterpret_cast<const double2 *>(pf_log_tab_dev) + i);
+#if defined(__CUDACC__)
+// Shared-memory copy of the table with the two hi-word constants expanded to
+// full doubles (32-byte entries: two loads and no register assembly per log).
+struct __align__(32) pf_log_wide {
+    double logc_hi, invc, logc_lo, pad;
+};
+__device__ __forceinline__ void pf_log_fill_wide(pf_log_wide *t, int tid, int nthreads) {
+    for (int i = tid; i < (1 << PF_LOG_BITS); i += nthreads) {
+        const pf_log_entry e = pf_log_tab_dev[i];
+        t[i] = {e.logc_hi, pf_log_dbl((uint64_t)e.invc_hi << 32), pf_log_dbl((uint64_t)e.logc_lo_hi << 32), 0.0};
     }
 }
 #endif
@@ -135,22 +134,26 @@ PF_LOG_HD double pf_log_scaled(double y, int escale, uint32_t tab = 0u) {
     const int kraw = (int32_t)tmp >> 20;
     const int k = kraw + escale;
     const uint32_t i = (tmp >> (20 - PF_LOG_BITS)) & ((1u << PF_LOG_BITS) - 1u);
+    double logc_hi, invc, logc_lo;
 #if defined(__CUDA_ARCH__)
-    pf_log_entry e;  // one 16-byte load
-    {
-        const double2 v = pf_log_tab_load<SMEM>(i, tab);
-        e.logc_hi = v.x;
+    if constexpr (SMEM) {  // pf_log_wide entries at byte address tab
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(logc_hi), "=d"(invc) : "r"(tab + 32u * i));
+        asm("ld.shared.f64 %0, [%1];" : "=d"(logc_lo) : "r"(tab + 32u * i + 16u));
+    } else {  // one 16-byte load of the compact entry
+        const double2 v = __ldg(reinterpret_cast<const double2 *>(pf_log_tab_dev) + i);
         const unsigned long long u = (unsigned long long)__double_as_longlong(v.y);
-        e.invc_hi = (uint32_t)u;
-        e.logc_lo_hi = (uint32_t)(u >> 32);
+        logc_hi = v.x;
+        invc = pf_log_dbl((uint64_t)(uint32_t)u << 32);
+        logc_lo = pf_log_dbl((u >> 32) << 32);
     }
 #else
     (void)tab;
     const pf_log_entry e = pf_log_tab_host[i];
+    logc_hi = e.logc_hi;
+    invc = pf_log_dbl((uint64_t)e.invc_hi << 32);
+    logc_lo = pf_log_dbl((uint64_t)e.logc_lo_hi << 32);
 #endif
     const double z = pf_log_dbl(((uint64_t)(hx - ((uint32_t)kraw << 20)) << 32) | (ix & 0xffffffffull));
-    const double invc = pf_log_dbl((uint64_t)e.invc_hi << 32);
-    const double logc_lo = pf_log_dbl((uint64_t)e.logc_lo_hi << 32);
 #if defined(__CUDA_ARCH__) && PF_LOG_I2F
     const double kd = __int2double_rn(k);  // exact; one I2F on the XU pipe (~20% busy) beats 3 ALU/DP ops
 #else
@@ -158,7 +161,7 @@ PF_LOG_HD double pf_log_scaled(double y, int escale, uint32_t tab = 0u) {
     const double kd = pf_log_sub(pf_log_dbl(0x4330000000000000ull | (uint32_t)(k + 1024)), 0x1.0000000000400p52);
 #endif
     const double r = pf_log_fma(z, invc, -1.0);                    // exact
-    const double w = pf_log_fma(kd, PF_LOG_C(7), e.logc_hi);       // exact
+    const double w = pf_log_fma(kd, PF_LOG_C(7), logc_hi);       // exact
     // TwoSum(w, r)
     const double hi = pf_log_add(w, r);
     const double bb = pf_log_sub(hi, w);

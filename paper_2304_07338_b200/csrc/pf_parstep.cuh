@@ -77,8 +77,8 @@ __device__ __forceinline__ ParFlight par_load(const ParFlightSmem &m, int tx) {
 // High word of the majorant bound of the cell holding x(t) (one TEX).
 __device__ __forceinline__ unsigned par_bound(const DevScene &S, const ParFlight &f, double t, double tb) {
     const float s = (float)(t - tb);
-    return tex3D<unsigned>(S.maj_tex, fmaf(f.qd[0], s, f.qo[0]), fmaf(f.qd[1], s, f.qo[1]),
-                           fmaf(f.qd[2], s, f.qo[2]));
+    return tex3DLod<unsigned>(S.maj_tex, fmaf(f.qd[0], s, f.qo[0]), fmaf(f.qd[1], s, f.qo[1]),
+                              fmaf(f.qd[2], s, f.qo[2]), 0.0f);
 }
 // u2sm >= 0: u2sm >= as_double(b, 0)  <=>  hi32(u2sm) >= b
 __device__ __forceinline__ bool par_null_given(double u2sm, unsigned b) {

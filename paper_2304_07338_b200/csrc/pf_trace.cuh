@@ -154,9 +154,8 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, PF_PAR_CTAS)
     const ParFlightSmem Fm{s_qa, s_qb};
     const int tx = threadIdx.x;
 #if PF_PAR_LOG_SMEM
-    __shared__ double2 s_logtab[1 << PF_LOG_BITS];
-    for (int i = tx; i < (1 << PF_LOG_BITS); i += PF_TRACE_THREADS)
-        s_logtab[i] = reinterpret_cast<const double2 *>(pf_log_tab_dev)[i];
+    __shared__ pf_log_wide s_logtab[1 << PF_LOG_BITS];
+    pf_log_fill_wide(s_logtab, tx, PF_TRACE_THREADS);
     __syncthreads();
     const uint32_t logtab = (uint32_t)__cvta_generic_to_shared(s_logtab);
 #define PAR_STEP(r) par_step_smem(r, inv_sm, logtab)
