@@ -408,8 +408,12 @@ def main():
         """The public API with HOST buffers: per-frame TF + lights in, the frame
         out to pinned host memory, host<->device copies inside the timed region."""
         host_frame = torch.empty((H_, W_, 3), dtype=torch.float32, pin_memory=True)
-        tf_h = torch.from_numpy(tf.copy()).pin_memory()
-        li_h = torch.from_numpy(lights.copy()).pin_memory()
+        # per-frame TF + lights: config 5's animation (the same scenes the device-
+        # timed loop renders), else the fixed scene re-sent every frame
+        scenes = [dynamic_scene(frame_no[0] + i, tf, lights) if CFG["dynamic"] else (tf, lights)
+                  for i in range(args.steps)]
+        tf_hs = [torch.from_numpy(np.ascontiguousarray(a).copy()).pin_memory() for a, _ in scenes]
+        li_hs = [torch.from_numpy(np.ascontiguousarray(b).copy()).pin_memory() for _, b in scenes]
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -422,8 +426,8 @@ def main():
             ctx.synchronize()
             t0 = time.perf_counter()
             for i in range(args.steps):
-                ctx.set_medium(tf_h.numpy(), 100.0)
-                ctx.set_lights(li_h.numpy())
+                ctx.set_medium(tf_hs[i].numpy(), 100.0)
+                ctx.set_lights(li_hs[i].numpy())
                 ctx.render_neural_async(cam, rc_, hosts[i % 2].numpy())
                 if i > 0:
                     ctx.frame_wait(hosts[(i - 1) % 2].numpy())
@@ -433,8 +437,8 @@ def main():
             times = []
             for i in range(args.steps):
                 t0 = time.perf_counter()
-                ctx.set_medium(tf_h.numpy(), 100.0)
-                ctx.set_lights(li_h.numpy())
+                ctx.set_medium(tf_hs[i].numpy(), 100.0)
+                ctx.set_lights(li_hs[i].numpy())
                 step(rc_, stats=False)
                 if rank == 0:
                     host_frame.copy_(frame, non_blocking=True)
