@@ -19,6 +19,7 @@
 // the tensor pipe and the gather units overlap.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -458,7 +459,7 @@ int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_b
     const size_t fixed = h.image.size() + 2048;  // + mbarriers (<= 1 + 17 x 8) and the TMEM slot
     // preferred: 8 warpgroups x one 16 KB tile (8 tiles in flight per SM, TMEM
     // 8 x 64 columns); else up to 4 warpgroups x two 16 KB chunk buffers.
-    // PF_MLP_WG=4 forces the double-buffered 4-warpgroup layout (A/B).
+    // PF_MLP_WG=1..4 forces that many double-buffered warpgroups (A/B).
     const char *e = std::getenv("PF_MLP_WG");
     const int want = e ? std::atoi(e) : 8;
     n_wg = 0;
@@ -466,7 +467,7 @@ int field_launch_config(const FieldHost &h, int &n_wg, size_t &smem, size_t &a_b
         n_wg = 8;
         a_bytes = 16384;
     } else {
-        for (int k = 4; k >= 1; --k)
+        for (int k = std::min(4, std::max(1, want)); k >= 1; --k)
             if (fixed + k * 32768 <= (size_t)max_smem) {
                 n_wg = k;
                 break;
