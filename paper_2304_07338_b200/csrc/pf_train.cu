@@ -42,6 +42,9 @@ namespace {
 // per SM) so an SM still runs 16 warps; 128 registers per thread fit.
 constexpr int kThreads = 512;
 constexpr int kChunk = 256;  // queries per weight-gradient partial
+#ifndef PF_TRAIN_SMEM_SCATTER
+#define PF_TRAIN_SMEM_SCATTER 1
+#endif
 
 __device__ __forceinline__ float relu(float x) { return x < 0.f ? 0.f : x; }
 
@@ -221,13 +224,90 @@ __device__ __forceinline__ void level_scatter(const TrainParams &T, int lv, cons
     }
 }
 
-// grid (query blocks, levels): blockIdx.y is the level, so the CTAs of one
-// level run together and its fixed-point gradient slab stays in L2
+// Coarse dense levels (<= kSmemSlots gradient words: e.g. the paper field's
+// pos levels 0-1 and dir levels 0-2) are the hottest atomic targets -- every
+// query of the batch hits the same few hundred entries.  A CTA first sums its
+// queries' contributions in shared memory, then adds each nonzero word to
+// the table once: the same integer total (fixed-point adds are associative,
+// so the step stays bit-reproducible) with ~256x fewer global atomics.
+constexpr int kSmemSlots = 6144;  // 48 KB of int64
+struct SmallLevels {
+    int n;
+    int lv[16];
+};
+// at most 16 small levels take the shared-memory path; any further ones stay on the global path
+
+template <int D, int F>
+__device__ __forceinline__ void level_scatter_smem(const TrainParams &T, int lv, const float *pin, int k0, size_t q,
+                                                   bool live, uint32_t entry_base, uint32_t tab_base, int Fdiv,
+                                                   unsigned long long *acc, uint32_t words) {
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) acc[i] = 0ull;
+    __syncthreads();
+    const FieldLevel L = T.lv[lv];
+    if (live) {
+        float dfeat[F];
+#pragma unroll
+        for (int k = 0; k < F; ++k) dfeat[k] = T.dF[(size_t)(k0 + k) * T.ld + q];
+        uint32_t c[D];
+        float f[D];
+        level_cell<D>(L, pin, c, f);
+#pragma unroll
+        for (int corner = 0; corner < (1 << D); ++corner) {
+            const float w = corner_weight<D>(f, corner);
+            const uint32_t idx = corner_index<D>(L, c, corner);
+#pragma unroll
+            for (int k = 0; k < F; ++k) {
+                const long long fx = __double2ll_rn((double)(w * dfeat[k]) * kGradFix);
+                if (fx != 0) atomicAdd(acc + (size_t)idx * F + k, (unsigned long long)fx);
+            }
+            T.touched[entry_base + (L.offset_halves - tab_base) / (uint32_t)Fdiv + idx] = 1;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+        if (acc[i] != 0ull) atomicAdd(T.gtab + L.offset_halves + i, acc[i]);
+}
+
+// Level lv of the table is "small": dense with <= kSmemSlots gradient words.
+__host__ __device__ __forceinline__ bool scatter_small(const TrainParams &T, int lv, int FP, int FD) {
+    const FieldLevel L = T.lv[lv];
+    const int D = lv < T.n_pos_levels ? 3 : 2, F = lv < T.n_pos_levels ? FP : FD;
+    uint64_t ent = 1;
+    for (int a = 0; a < D; ++a) ent *= L.n1;
+    return L.dense && ent * (uint64_t)F <= (uint64_t)kSmemSlots;
+}
+
+// the small levels: one CTA per (256 queries, small level), smem pre-sum
 template <int FP, int FD>
-__global__ void __launch_bounds__(256) k_train_scatter(const TrainParams T) {
+__global__ void __launch_bounds__(256) k_train_scatter_small(const TrainParams T, const SmallLevels SL) {
+    __shared__ unsigned long long acc[kSmemSlots];
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= T.n) return;
+    const int lv = SL.lv[blockIdx.y];
+    const FieldLevel L = T.lv[lv];
+    const bool live = q < T.n;
+    const size_t qq = live ? q : 0;
+    if (lv < T.n_pos_levels) {
+        const uint32_t words = L.n1 * L.n1 * L.n1 * (uint32_t)FP;
+        const float pin[3] = {__saturatef(T.qx[3 * qq]), __saturatef(T.qx[3 * qq + 1]), __saturatef(T.qx[3 * qq + 2])};
+        level_scatter_smem<3, FP>(T, lv, pin, lv * FP, qq, live, 0u, 0u, FP, acc, words);
+    } else {
+        const int l = lv - T.n_pos_levels;
+        const uint32_t words = L.n1 * L.n1 * (uint32_t)FD;
+        const float pin[2] = {__saturatef(T.qw[2 * qq]), __saturatef(T.qw[2 * qq + 1])};
+        level_scatter_smem<2, FD>(T, lv, pin, T.n_pos_levels * FP + l * FD, qq, live, T.n_pos_tab / (uint32_t)FP,
+                                  T.n_pos_tab, FD, acc, words);
+    }
+}
+
+// grid (query blocks, levels): blockIdx.y is the level, so the CTAs of one
+// level run together and its fixed-point gradient slab stays in L2 (small
+// levels are k_train_scatter_small's)
+template <int FP, int FD>
+__global__ void __launch_bounds__(256) k_train_scatter(const TrainParams T, uint32_t small_mask) {
+    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lv = blockIdx.y;
+    if ((small_mask >> lv) & 1u) return;  // CTA-uniform: done by k_train_scatter_small
+    if (q >= T.n) return;
     if (lv < T.n_pos_levels) {
         const float pin[3] = {__saturatef(T.qx[3 * q]), __saturatef(T.qx[3 * q + 1]), __saturatef(T.qx[3 * q + 2])};
         level_scatter<3, FP>(T, lv, pin, lv * FP, q, 0u, 0u, FP);
@@ -487,8 +567,21 @@ cudaError_t launch_fb(const TrainParams &T, const float4 *img, int n4, size_t sm
         k_train_bwd<FP, FD><<<blocks, kThreads, smem, st>>>(T, img, n4);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        const dim3 sg((unsigned)((T.n + 255) / 256), (unsigned)(T.n_pos_levels + T.n_dir_levels));
-        k_train_scatter<FP, FD><<<sg, 256, 0, st>>>(T);
+        SmallLevels SL{};
+        SL.n = 0;
+#if PF_TRAIN_SMEM_SCATTER
+        for (int lv = 0; lv < T.n_pos_levels + T.n_dir_levels && SL.n < 16; ++lv)
+            if (scatter_small(T, lv, FP, FD)) SL.lv[SL.n++] = lv;
+#endif
+        const unsigned qb = (unsigned)((T.n + 255) / 256);
+        if (SL.n > 0) {
+            k_train_scatter_small<FP, FD><<<dim3(qb, (unsigned)SL.n), 256, 0, st>>>(T, SL);
+            const cudaError_t e2 = cudaGetLastError();
+            if (e2 != cudaSuccess) return e2;
+        }
+        uint32_t small_mask = 0u;
+        for (int i = 0; i < SL.n; ++i) small_mask |= 1u << SL.lv[i];
+        k_train_scatter<FP, FD><<<dim3(qb, (unsigned)(T.n_pos_levels + T.n_dir_levels)), 256, 0, st>>>(T, small_mask);
     }
     return cudaGetLastError();
 }
