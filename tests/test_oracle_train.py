@@ -112,3 +112,29 @@ def test_checkpoint_file_roundtrip(tmp_path):
     with pytest.raises(ValueError):
         load_checkpoint(f)
     assert [lr_at(s, 3000) for s in (0, 2125, 3000)] == pytest.approx([9e-4, 8.28e-4, 4.473055573e-5], rel=1e-9)
+
+
+def test_checkpoint_version1_still_loads(tmp_path):
+    """Round-1 checkpoints (version 1: no Adam block) load; their Adam config
+    and total_steps read as unknown (None, 0)."""
+    import struct
+    from paper_2304_07338_b200 import checkpoint_training_state, load_checkpoint
+    fc = FieldConfig.desk()
+    p = fc.init_params(seed=4, embed_scale=0.1)
+    m, v = p * 0.25, np.abs(p) * 1e-4
+    gs = np.array([-0.75, 0.0, 0.75])
+    f = tmp_path / "v1.pffc"
+    with open(f, "wb") as fh:  # the version-1 layout, written by hand
+        fh.write(b"PFFC" + struct.pack("<I", 1))
+        for hg in (fc.pos, fc.dir):
+            fh.write(struct.pack("<iiiidi", hg.dims, hg.levels, hg.features, hg.base_res, float(hg.growth),
+                                 hg.log2_table))
+        fh.write(struct.pack("<iid", fc.hidden_layers, fc.width, float(fc.psi)))
+        fh.write(struct.pack("<I", len(gs)) + gs.astype("<f8").tobytes())
+        fh.write(struct.pack("<QQ", 7, len(p)))
+        for arr in (p, m, v):
+            fh.write(np.asarray(arr, np.float64).astype("<f8").tobytes())
+    cfg, g2, step, p2, m2, v2 = load_checkpoint(f)
+    assert cfg == fc and g2 == list(gs) and step == 7
+    assert np.array_equal(p2, p.astype(np.float64)) and np.array_equal(v2, v.astype(np.float64))
+    assert checkpoint_training_state(f) == (None, 0)
