@@ -642,7 +642,7 @@ static FieldParams field_params(pf_ctx *c) {
     for (int i = 0; i < 8; ++i) P.off_w[i] = h.off_w[i];
     P.off_bias = h.off_bias;
     P.psi_log2_10 = (float)(h.psi * 3.3219280948873623478703194294894);
-    for (size_t i = 0; i < h.levels.size(); ++i) P.lv[i] = h.levels[i];
+    for (size_t i = 0; i < h.enc_levels.size(); ++i) P.lv[i] = h.enc_levels[i];
     P.tables = (const __half *)c->f_tables.p;
     P.img = c->f_img.p;
     P.nch = (h.K0 + field_chunk_cols() - 1) / field_chunk_cols();

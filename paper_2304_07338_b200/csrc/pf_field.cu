@@ -78,6 +78,9 @@ static_assert(PF_ENC_G == 2 || PF_ENC_G == 4 || PF_ENC_G == 8, "levels per encod
 // 3% / 9%, the hash tables in use stay L2-resident) so each level's rows land
 // as contiguous 128-byte stores.  Units: pos levels, dir levels, then one
 // "g + zero padding" unit.  6 CTAs of 256 per SM (40 registers).
+#ifndef PF_ENC_PF
+#define PF_ENC_PF 0
+#endif
 #ifndef PF_ENC_MINB
 #define PF_ENC_MINB 6
 #endif
@@ -108,6 +111,11 @@ __global__ void __launch_bounds__(256, PF_ENC_MINB) k_field_encode(const FieldPa
         if (u >= U) continue;
         const bool valid = row < n;
         const size_t gr = P.row0 + row;  // global item index
+#if PF_ENC_PF
+        // pull the warp's next hit records toward L2 while this group's gathers run
+        if (P.mode == 0 && rg + n_warps < n_rg && lane < RW)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.hits + gr + (size_t)n_warps * RW));
+#endif
         float x[3] = {0.f, 0.f, 0.f}, ws[2] = {0.f, 0.f}, gin = 0.f;
         if (valid) {
             if (P.mode == 0) {
@@ -400,12 +408,12 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
     out.fd = d.dir.features;
     out.hidden_layers = d.hidden_layers;
     out.psi = d.psi;
-    // --- tables -> fp16, same order as the flat vector
-    const size_t ntab = field_grid_param_count(d.pos) + field_grid_param_count(d.dir);
-    out.tables.resize(ntab);
-    for (size_t i = 0; i < ntab; ++i) out.tables[i] = __half_as_ushort(__float2half_rn(params[i]));
+    // --- tables -> fp16, same order as the flat vector; every level starts on
+    // an even entry so the encoder can fetch an x-adjacent corner pair (2F
+    // halves, one 32-byte sector at F = 8) with one load
     out.levels.clear();
-    size_t off = 0;
+    out.enc_levels.clear();
+    size_t off = 0, eoff = 0;
     for (const FieldGridDesc *g : {&d.pos, &d.dir}) {
         for (int l = 0; l < g->levels; ++l) {
             FieldLevel L{};
@@ -416,9 +424,19 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
             L.mask = (1u << g->log2_table) - 1u;
             L.offset_halves = (uint32_t)off;
             out.levels.push_back(L);
+            L.offset_halves = (uint32_t)eoff;
+            out.enc_levels.push_back(L);
             off += (size_t)v * g->features;
+            eoff += (size_t)((v + 1) & ~(uint64_t)1) * g->features;
         }
     }
+    out.tables.assign(eoff, 0);
+    for (size_t l = 0; l < out.levels.size(); ++l) {
+        const size_t src = out.levels[l].offset_halves, dst = out.enc_levels[l].offset_halves;
+        const size_t end = l + 1 < out.levels.size() ? out.levels[l + 1].offset_halves : off;
+        for (size_t k = 0; k < end - src; ++k) out.tables[dst + k] = __half_as_ushort(__float2half_rn(params[src + k]));
+    }
+    const size_t ntab = off;
     // --- MLP image: W_0..W_H (canonical fp16), then fp32 biases
     const float *mlp = params + ntab;
     const int H = d.hidden_layers;

@@ -64,8 +64,9 @@ struct FieldParams {
 struct FieldHost {
     int K0 = 0, n_pos_levels = 0, n_dir_levels = 0, fp = 0, fd = 0, hidden_layers = 0;
     double psi = 5.0;
-    std::vector<uint16_t> tables;  // fp16 bits
-    std::vector<FieldLevel> levels;
+    std::vector<uint16_t> tables;  // fp16 bits, each level padded to an even entry count
+    std::vector<FieldLevel> levels;      // offset_halves into the flat fp32 parameter vector (trainer)
+    std::vector<FieldLevel> enc_levels;  // offset_halves into `tables` (encoder, pair-aligned)
     std::vector<uint8_t> image;    // smem image (weights canonical fp16 + fp32 biases)
     uint32_t off_w[8] = {0};
     uint32_t off_bias = 0;
