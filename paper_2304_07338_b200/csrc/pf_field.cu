@@ -78,9 +78,6 @@ static_assert(PF_ENC_G == 2 || PF_ENC_G == 4 || PF_ENC_G == 8, "levels per encod
 // 3% / 9%, the hash tables in use stay L2-resident) so each level's rows land
 // as contiguous 128-byte stores.  Units: pos levels, dir levels, then one
 // "g + zero padding" unit.  6 CTAs of 256 per SM (40 registers).
-#ifndef PF_ENC_PF
-#define PF_ENC_PF 0
-#endif
 #ifndef PF_ENC_MINB
 #define PF_ENC_MINB 6
 #endif
@@ -111,11 +108,6 @@ __global__ void __launch_bounds__(256, PF_ENC_MINB) k_field_encode(const FieldPa
         if (u >= U) continue;
         const bool valid = row < n;
         const size_t gr = P.row0 + row;  // global item index
-#if PF_ENC_PF
-        // pull the warp's next hit records toward L2 while this group's gathers run
-        if (P.mode == 0 && rg + n_warps < n_rg && lane < RW)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.hits + gr + (size_t)n_warps * RW));
-#endif
         float x[3] = {0.f, 0.f, 0.f}, ws[2] = {0.f, 0.f}, gin = 0.f;
         if (valid) {
             if (P.mode == 0) {
@@ -409,8 +401,10 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
     out.hidden_layers = d.hidden_layers;
     out.psi = d.psi;
     // --- tables -> fp16, same order as the flat vector; every level starts on
-    // an even entry so the encoder can fetch an x-adjacent corner pair (2F
-    // halves, one 32-byte sector at F = 8) with one load
+    // a 32-byte boundary, so the two entries of an x-edge whose first index is
+    // even (dense: x even in the flattened index; hashed: cell x even, since
+    // x ^ 1 flips only bit 0 of the hash) share one 32-byte sector at F = 8,
+    // and F-wide vector loads of either grid stay aligned for any (Fp, Fd)
     out.levels.clear();
     out.enc_levels.clear();
     size_t off = 0, eoff = 0;
@@ -427,7 +421,7 @@ void field_pack(const FieldDesc &d, const float *params, FieldHost &out) {
             L.offset_halves = (uint32_t)eoff;
             out.enc_levels.push_back(L);
             off += (size_t)v * g->features;
-            eoff += (size_t)((v + 1) & ~(uint64_t)1) * g->features;
+            eoff = (eoff + (size_t)v * g->features + 15) & ~(size_t)15;
         }
     }
     out.tables.assign(eoff, 0);

@@ -80,44 +80,12 @@ __device__ __forceinline__ void issue_layer(uint32_t a_s, uint32_t b_s, int K, i
     }
 }
 
-// Two consecutive table entries (2F fp16) starting at an even entry: one
-// 256-bit load at F = 8 (LDG.256, one 32-byte sector).
-template <int F>
-struct Pair {
-    Raw<F> lo, hi;
-};
-
-template <int F>
-__device__ __forceinline__ Pair<F> load_pair(const __half *tab, uint32_t e_even) {
-    Pair<F> r;
-    const __half *q = tab + (size_t)e_even * F;
-    if constexpr (F == 8) {
-        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(r.lo.v.x), "=r"(r.lo.v.y), "=r"(r.lo.v.z), "=r"(r.lo.v.w), "=r"(r.hi.v.x), "=r"(r.hi.v.y),
-              "=r"(r.hi.v.z), "=r"(r.hi.v.w)
-            : "l"(q));
-    } else if constexpr (F == 4) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(q));
-        r.lo.v = make_uint2(v.x, v.y), r.hi.v = make_uint2(v.z, v.w);
-    } else {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(q));
-        r.lo.v = v.x, r.hi.v = v.y;
-    }
-    return r;
-}
-
-#ifndef PF_ENC_PAIR
-#define PF_ENC_PAIR 0  // A/B on C2: field 1.29 ms (pair loads, 4 CTAs/SM; 6 CTAs spill) vs 1.22 ms (off)
-#endif
-
 // Encode ONE level of one input (pinned in oracle
-// or_hashgrid_encode): 2^D gathers issued back to back, fp32 accumulation in
-// corner order.  PF_ENC_PAIR: the two corners of an x-edge are fetched by one
-// pair load when they are the two entries of one aligned pair -- always for a
-// dense level with an even first index (x + 1 -> index + 1), and for a hashed
-// level when the cell's x is even (x ^ 1 flips only bit 0 of the hash) -- else
-// the second corner is one extra (predicated) load: 1.5 instead of 2 sectors
-// per edge on average, same values, same summation order.
+// or_hashgrid_encode): 2^D gathers issued back to back, fp32 accumulation.
+// (Tried: one 256-bit load per x-edge corner pair when both entries share an
+// aligned pair, else a predicated second load -- 1.5 instead of 2 sectors per
+// edge, but it spills at 40 registers and at 4 CTAs/SM the field took 1.29 ms
+// vs 1.22 ms; reverted.)
 template <int D, int F>
 __device__ __forceinline__ void encode_level(const __half *tables, const FieldLevel L, const float *pin, float *acc) {
     constexpr int NC = 1 << D;
@@ -125,29 +93,6 @@ __device__ __forceinline__ void encode_level(const __half *tables, const FieldLe
     float f[D];
     level_cell<D>(L, pin, c, f);
     const __half *tab = tables + L.offset_halves;
-#if PF_ENC_PAIR
-    constexpr int NP = NC / 2;
-    Pair<F> p[NP];
-    Raw<F> s[NP];
-    bool odd[NP], same[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-        const uint32_t e0 = corner_index<D>(L, c, 2 * k), e1 = corner_index<D>(L, c, 2 * k + 1);
-        odd[k] = (e0 & 1u) != 0u;
-        same[k] = e1 == (e0 ^ 1u);
-        p[k] = load_pair<F>(tab, e0 & ~1u);
-        if (!same[k]) s[k] = load_raw<F>(tab, e1);
-    }
-#pragma unroll
-    for (int k = 0; k < F; ++k) acc[k] = 0.f;
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-        const Raw<F> a = odd[k] ? p[k].hi : p[k].lo;
-        const Raw<F> b = same[k] ? (odd[k] ? p[k].lo : p[k].hi) : s[k];
-        accum_raw<F>(a, corner_weight<D>(f, 2 * k), acc);
-        accum_raw<F>(b, corner_weight<D>(f, 2 * k + 1), acc);
-    }
-#else
     Raw<F> e[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) e[k] = load_raw<F>(tab, corner_index<D>(L, c, k));
@@ -155,7 +100,6 @@ __device__ __forceinline__ void encode_level(const __half *tables, const FieldLe
     for (int k = 0; k < F; ++k) acc[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) accum_raw<F>(e[k], corner_weight<D>(f, k), acc);
-#endif
 }
 
 template <int D, int F>
