@@ -25,6 +25,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 SOURCES = {
     "pf_trace_parity.cu": ["--fmad=false"],
     "pf_trace_fast.cu": [],
+    "pf_trace_fast_batch.cu": ["-Xptxas", "-O1"],  # ptxas -O3 miscompiles its DDA walk (see the file)
     "pf_pathtrace_parity.cu": ["--fmad=false"],
     "pf_pathtrace_fast.cu": [],
     "pf_field.cu": [],

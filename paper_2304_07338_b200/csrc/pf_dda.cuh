@@ -50,9 +50,13 @@ __device__ __forceinline__ void dda_init(const DevScene &S, const float o[3], co
 // Spend optical depth tau through the majorant grid from t.  Returns true at a
 // tentative collision (t updated, m = that cell's majorant); false when the
 // flight reaches t1 first.
+// kGuard: also stop the flight if the linear cell index ever leaves the grid
+// (the batch entries; see pf_trace_fast_batch.cu).
+template <bool kGuard = false>
 __device__ __forceinline__ bool dda_advance(const DevScene &S, Dda &D, float &t, float t1, float &tau, float &m) {
     const int stride_y = S.mc[0], stride_z = S.mc[0] * S.mc[1];
     for (;;) {
+        if (kGuard && (unsigned)D.cell >= (unsigned)(stride_z * S.mc[2])) return false;
         m = __ldg(S.maj + D.cell);
         const float tn = fminf(D.tmx, fminf(D.tmy, D.tmz));
         const float t_exit = fminf(tn, t1);

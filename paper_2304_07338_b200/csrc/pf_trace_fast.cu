@@ -1,4 +1,5 @@
-// pf_trace_fast.cu -- FAST-mode render tracer (binary32) + fast batch entries.
+// pf_trace_fast.cu -- FAST-mode render tracer (binary32); the batch entries
+// are in pf_trace_fast_batch.cu.
 //
 // Same persistent lane state machine and the same per-sample RNG streams as
 // the parity tracer (pf_trace.cuh), but the majorant is piecewise constant
@@ -192,101 +193,6 @@ __global__ void __launch_bounds__(PF_TRACE_THREADS, 8) k_render_trace_fast(const
 
 cudaError_t launch_render_trace_fast(const DevScene &S, const TraceParams &P, int grid, cudaStream_t st) {
     k_render_trace_fast<<<grid, PF_TRACE_THREADS, 0, st>>>(S, P);
-    return cudaGetLastError();
-}
-
-// FAST-mode batch entries (DDA majorants): what the render tracer does per
-// flight, exposed for statistical tests against the parity kernels.
-__global__ void k_delta_track_batch_dda(const DevScene S, BatchParams B) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B.n) return;
-    Pcg rng;
-    pcg_init(rng, B.initstate, B.idx[i]);
-    float o[3], d[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        o[a] = (float)B.a3[3 * i + a];
-        d[a] = (float)B.b3[3 * i + a];
-    }
-    float t, t1;
-    B.hit[i] = 0;
-    if (B.scalar) B.scalar[i] = 0.0;
-    if (!aabb_unit<float>(o, d, (float)B.tmin[i], (float)B.tmax[i], t, t1) || !(S.sigma_max_f > 0.f) ||
-        !occ_clip(S, o, d, t, t1))
-        return;
-    Dda D;
-    dda_init(S, o, d, t, D);
-    float tau = sample_tau(rng), m;
-    while (dda_advance(S, D, t, t1, tau, m)) {
-        float x[3] = {fmaf(d[0], t, o[0]), fmaf(d[1], t, o[1]), fmaf(d[2], t, o[2])};
-        const float s = sample_f(S, x);
-        if (pcg_u_f(rng) * m < S.density_scale_f * tf_alpha_f(S, s)) {
-            B.hit[i] = 1;
-            if (B.pos3)
-                for (int a = 0; a < 3; ++a) B.pos3[3 * i + a] = (double)x[a];
-            if (B.scalar) B.scalar[i] = (double)s;
-            if (B.rgba4) {
-                float c[4];
-                tf_rgba_f(S, s, c);
-                for (int a = 0; a < 4; ++a) B.rgba4[4 * i + a] = (double)c[a];
-            }
-            return;
-        }
-        tau = sample_tau(rng);
-    }
-}
-
-__global__ void k_transmittance_ratio_dda(const DevScene S, BatchParams B) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B.n) return;
-    Pcg rng;
-    pcg_init(rng, B.initstate, B.idx[i]);
-    float a[3], dv[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        a[k] = (float)B.a3[3 * i + k];
-        dv[k] = (float)B.b3[3 * i + k] - a[k];
-    }
-    const float len = sqrtf(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
-    float dir[3] = {dv[0] / len, dv[1] / len, dv[2] / len};
-    float t0, t1;
-    if (len == 0.0f || !aabb_unit<float>(a, dir, 0.0f, len, t0, t1) || !(S.sigma_max_f > 0.0f) ||
-        !occ_clip(S, a, dir, t0, t1)) {
-        B.out[i] = 1.0;
-        return;
-    }
-    double acc = 0.0;
-    for (int trial = 0; trial < B.n_trials; ++trial) {
-        float t = t0, T = 1.0f, m;
-        Dda D;
-        dda_init(S, a, dir, t, D);
-        float tau = sample_tau(rng);
-        while (dda_advance(S, D, t, t1, tau, m)) {
-            float x[3] = {fmaf(dir[0], t, a[0]), fmaf(dir[1], t, a[1]), fmaf(dir[2], t, a[2])};
-            T *= 1.0f - S.density_scale_f * tf_alpha_f(S, sample_f(S, x)) / m;
-            if (T < 0.1f) {
-                if (pcg_u_f(rng) >= T * 10.0f) {
-                    T = 0.0f;
-                    break;
-                }
-                T = 0.1f;
-            }
-            tau = sample_tau(rng);
-        }
-        acc += (double)T;
-    }
-    B.out[i] = acc / B.n_trials;
-}
-
-cudaError_t launch_delta_track_batch_fast(const DevScene &S, const BatchParams &B, cudaStream_t st) {
-    const unsigned blocks = (unsigned)((B.n + 127) / 128);
-    k_delta_track_batch_dda<<<blocks, 128, 0, st>>>(S, B);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_transmittance_ratio_batch(const DevScene &S, const BatchParams &B, cudaStream_t st) {
-    const unsigned blocks = (unsigned)((B.n + 127) / 128);
-    k_transmittance_ratio_dda<<<blocks, 128, 0, st>>>(S, B);
     return cudaGetLastError();
 }
 

@@ -153,3 +153,36 @@ def test_ratio_tracking_unbiased(scene):
     t_delta = ctx.transmittance_batch(a, b, 4, "nee", idx, 20000)
     se = np.sqrt(np.maximum(t_delta * (1 - t_delta), 1e-4) / 20000) * 2
     assert np.all(np.abs(t_ratio - t_delta) < 5 * se + 2e-3)
+
+
+def test_fast_batch_independent_of_allocation_placement(oracle):
+    """Regression: ptxas -O3 once miscompiled the FAST batch DDA walk so that
+    some flights read majorants out of bounds -- results then depended on where
+    the buffers were allocated (and faulted once the process held enough
+    memory).  The same rays must give the same flights with the buffers placed
+    low and after 64 GiB of other allocations."""
+    import torch
+    from paper_2304_07338_b200 import Context
+    from paper_2304_07338_b200.scene import synth_volume, tf_scene_a
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80 * 2**30:
+        pytest.skip("needs ~80 GiB of free device memory")
+    n = 200000
+    r = np.random.default_rng(8)
+    o = np.tile([0.5, 0.5, -0.9], (n, 1))
+    d = np.column_stack([r.uniform(-0.3, 0.3, n), r.uniform(-0.3, 0.3, n), np.ones(n)])
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    idx = np.arange(n, dtype=np.uint64)
+    vol = synth_volume("sphere_sinusoid", 64)
+    out = []
+    for hold_gib in (0, 64):
+        hold = torch.empty(hold_gib * 2**30, dtype=torch.uint8, device="cuda") if hold_gib else None
+        with Context(0) as c:
+            c.upload_volume(vol)
+            c.set_medium(tf_scene_a(), 100.0)
+            h, p, _ = c.delta_track_batch(o, d, np.zeros(n), np.full(n, np.inf), 5, "camera", idx, fp64=False)
+        out.append((h.copy(), p.copy()))
+        del hold
+        torch.cuda.empty_cache()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1][out[0][0] == 1], out[1][1][out[1][0] == 1])

@@ -9,6 +9,9 @@ import bench  # noqa: E402
 from paper_2304_07338_b200 import Context, FieldConfig, RenderConfig  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "fast"
+# optional: hold <GB> of device memory first (allocation placement must not change the frame)
+import torch  # noqa: E402
+_hold = torch.empty(int(float(sys.argv[2]) * 2**30), dtype=torch.uint8, device="cuda") if len(sys.argv) > 2 else None
 vol, tf, lights, cam = bench.scene_inputs()
 with Context(0) as ctx:
     ctx.upload_volume(vol)
