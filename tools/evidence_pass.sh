@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 evidence pass (one gpurun call): full GPU suite, the driver's bench
+# Evidence pass (one gpurun call): full GPU suite, the driver's bench
 # lines (ours, reference arm, C4, C5), the launch list, and ncu captures of
 # every hot kernel, summarised on the box.  Timing numbers come from bench.py only.
 export PYTHONPATH=$PWD
