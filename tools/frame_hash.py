@@ -19,5 +19,8 @@ with Context(0) as ctx:
     ctx.set_lights(lights)
     fc = FieldConfig.paper()
     ctx.load_field(fc, fc.init_params(seed=bench.SEED, embed_scale=1e-2))
-    img = ctx.render_neural(cam, RenderConfig(spp=bench.SPP, seed=bench.SEED, mode=mode))
+    rm = mode.replace("pt_", "")
+    rc = RenderConfig(spp=bench.SPP, seed=bench.SEED, mode=rm)
+    # "pt_fast" / "pt_parity": render_path_traced (its FAST walk shares the DDA)
+    img = ctx.render_path_traced(cam, rc) if mode.startswith("pt_") else ctx.render_neural(cam, rc)
 print(mode, hashlib.sha256(img.tobytes()).hexdigest()[:16], float(img.mean()))
