@@ -539,6 +539,10 @@ __device__ __forceinline__ void select_topk(uint64_t *buf, int n, unsigned lane)
     __syncwarp();
 }
 
+#ifndef PF_KNN_EARLY
+#define PF_KNN_EARLY 1
+#endif
+
 template <int KP>
 __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnParams P) {
     __shared__ uint64_t s_keys[kSelWarps][kSelCap];
@@ -666,6 +670,12 @@ __global__ void __launch_bounds__(kSelWarps * 32, 8) k_knn_query_sel(const KnnPa
                     }
                     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
                     for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+#if PF_KNN_EARLY
+                        // the ball already overflowed the buffer: this attempt will be
+                        // retried with a smaller ball, stop scanning (n is then a lower
+                        // bound of the ball's count, so the shrink is conservative)
+                        if (n > kSelCap) break;
+#endif
                         const uint32_t t = t0 + lane;
                         // segment of candidate t: first lane whose inclusive offset exceeds t
                         int pos = 0;
@@ -964,6 +974,10 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                     const float gz = gap(2, cz, cz);
                     if ((gz + gx) * (1.0f - 1e-5f) > thr) continue;
                     for (int cy = y0; cy <= y1; ++cy) {
+#if PF_KNN_EARLY
+                        // the ball already overflowed the buffer: the attempt is retried
+                        if (*(volatile int *)&s_over) break;
+#endif
                         const float gyz = gz + gap(1, cy, cy);
                         if ((gyz + gx) * (1.0f - 1e-5f) > thr) continue;
                         const float dxm = sqrtf(fmaxf(thr - gyz * (1.0f - 1e-5f), 0.0f)) * 1.0001f + eps;
@@ -973,6 +987,9 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                         const uint32_t row = cbase + (uint32_t)R[0] * ((uint32_t)cy + (uint32_t)R[1] * (uint32_t)cz);
                         const uint32_t b = __ldg(P.cell_start + row + xa), e = __ldg(P.cell_start + row + xb + 1);
                         for (uint32_t j = b + lane; j < e; j += 32) {
+#if PF_KNN_EARLY
+                            if (*(volatile int *)&s_over) break;
+#endif
                             const float4 c = __ldg(&P.spos[j]);
                             const float d2 = d2_rn(c, q);
                             if (d2 <= thr) {
