@@ -872,6 +872,9 @@ __device__ __forceinline__ void cta_sort(uint64_t *a, int P2, int warp, unsigned
     }
 }
 constexpr int kCtaCap = 4096;  // collected keys per query (32 KB)
+#ifndef PF_KNN_CTA_TGT
+#define PF_KNN_CTA_TGT 2.5  // photons a K7c ball is sized to hold, in units of K (A/B: 1.3 / 2.0 / 2.5 / 3.0 -> 8.04 / 7.79 / 7.68 / 7.65 ms per 2^16 K=1024 targets; 2.5 keeps the expected count well inside the 4 K buffer)
+#endif
 
 __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParams P) {
     __shared__ uint64_t keys[kCtaCap];
@@ -939,7 +942,7 @@ __global__ void __launch_bounds__(kCtaThreads, 5) k_knn_query_cta(const KnnParam
                 const int c0 = max(qc[a] - ring, 0), c1 = min(qc[a] + ring, R[a] - 1);
                 vol *= (double)(c1 - c0 + 1) * (double)h[a];
             }
-            double rho = cbrt(1.3 * (double)K * vol / (fmax((double)cube, 1.0) * 4.18879020478639098));
+            double rho = cbrt(PF_KNN_CTA_TGT * (double)K * vol / (fmax((double)cube, 1.0) * 4.18879020478639098));
             // a radius whose ball holds every photon of the phase (grid box + slack)
             double all = 0.0;
 #pragma unroll
